@@ -1,0 +1,130 @@
+/* ffd.h — C ABI of the B200-native discrete Fréchet distance library (libffd.so).
+ *
+ * Method: arxiv 2404.05708 ("Walking Your Frog Fast in 4 LoC"), PAPER.md.
+ *   δ_dF(p, q) for curves p ∈ R^{P×D}, q ∈ R^{Q×D} is M_PQ of
+ *   the recurrence Eq. (1), M_ij = max{min{M_{i-1,j}, M_{i-1,j-1}, M_{i,j-1}}, d_ij}
+ *   (L159–L163), evaluated iteratively, branch-free and in linear memory
+ *   (Alg. 2 / Alg. 5) with d_ij = ‖p_i − q_j‖ evaluated
+ *   lazily (Theorem 1).  Batching over independent pairs follows PAPER
+ *   L259–L262 (padding by repeated points, sorting by length).
+ *
+ * General conventions (every entry point):
+ *   - Pointers named *_host are host memory; every other pointer is DEVICE memory
+ *     owned by the caller.  Nothing is retained after the call returns.
+ *   - Calls are asynchronous on `stream` (a cudaStream_t; NULL = legacy default
+ *     stream) unless stated otherwise, reentrant and thread-safe.
+ *   - Host-checkable argument errors return a status synchronously and launch
+ *     nothing.  CUDA launch failures return FFD_ERR_CUDA.  Device-data
+ *     preconditions (lengths ≥ 1, offsets in range, finite coordinates) are NOT
+ *     checked by the asynchronous calls; ffd_validate_batch checks them.  A pair
+ *     with a length < 1 gets NaN (fp32) / INT64_MIN (int) and reads nothing.
+ *   - Integer inputs give exact results: every int32-coordinate result equals the
+ *     exact int64 value whenever D·(max |coordinate difference|)² ≤ 2^63 − 1.
+ *   - fp32 inputs: per-cell distances in fp32 with the operation order given in
+ *     DESIGN.md §"fp32 arithmetic"; L2 takes one square root at the end (exact:
+ *     sqrt is monotone).  Relative error ≤ 1e-5 of the exact value.
+ */
+#ifndef FFD_H
+#define FFD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* ffd_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  FFD_OK = 0,
+  FFD_ERR_ARG = -1,         /* bad argument (null pointer, bad dim/norm/dtype, sizes) */
+  FFD_ERR_UNSUPPORTED = -2, /* valid request the library does not implement */
+  FFD_ERR_CUDA = -3,        /* a CUDA call failed */
+  FFD_ERR_EMPTY = -4,       /* validate: a curve has length < 1 */
+  FFD_ERR_NONFINITE = -5,   /* validate: NaN / ±Inf coordinate */
+  FFD_ERR_OVERFLOW = -6,    /* validate: int32 input with D·range² > 2^63 − 1 */
+  FFD_ERR_RANGE = -7,       /* validate: offsets + lengths outside the point arrays */
+  FFD_ERR_WORKSPACE = -8    /* workspace smaller than the *_workspace_bytes() value */
+} ffd_status;
+
+typedef enum {
+  FFD_L1 = 1,   /* Σ|Δ_k|                                   */
+  FFD_L2 = 2,   /* sqrt(Σ Δ_k²) — Euclidean      */
+  FFD_LINF = 3, /* max |Δ_k|                                  */
+  FFD_SQL2 = 4  /* Σ Δ_k²  (squared Euclidean; same coupling as L2) */
+} ffd_norm;
+
+typedef enum {
+  FFD_F32 = 0, /* coordinates float32; out float32                          */
+  FFD_I32 = 1  /* coordinates int32; out int64 (norms SQL2, L1, LINF only)   */
+} ffd_dtype;
+
+/* ---------------------------------------------------------------------------
+ * ffd_batch — discrete Fréchet distance of B independent curve pairs.
+ *   out[k] = δ_dF(p[offsets[k] .. offsets[k]+lengths[k]),
+ *                 q[offsets[B+k] .. offsets[B+k]+lengths[B+k]])   under `norm`.
+ *   p: [Σn, dim] points, q: [Σm, dim] points, array-of-structures, row-major,
+ *      element type per `dtype`, naturally aligned.
+ *   offsets: int64[2B] (in points; first the B p-offsets, then the B q-offsets).
+ *   lengths: int32[2B] (same order), each ≥ 1 by precondition.
+ *   dim ∈ {1,2,3,4}.  out: float[B] (FFD_F32) or int64[B] (FFD_I32).
+ *   workspace: device scratch of at least ffd_batch_workspace_bytes(B) bytes,
+ *   16-byte aligned, owned by the caller, not read before being written.
+ *   Pairs are processed in an order sorted by length; the
+ *   result does not depend on that order.
+ * ------------------------------------------------------------------------- */
+int ffd_batch(const void* p, const void* q, const int64_t* offsets, const int32_t* lengths,
+              int64_t num_pairs, int32_t dim, int32_t norm, int32_t dtype, void* out,
+              void* workspace, size_t workspace_bytes, ffd_stream_t stream);
+size_t ffd_batch_workspace_bytes(int64_t num_pairs);
+
+/* ffd_batch_host — the same computation from HOST buffers (end-to-end path).
+ *   p_host: [np, dim], q_host: [nq, dim]; offsets_host/lengths_host as above;
+ *   out_host: float[B] / int64[B].  Host buffers should be pinned for overlap.
+ *   Copies in, computes and copies out on `stream` using device memory from a
+ *   stream-ordered pool; synchronises `stream` before returning.              */
+int ffd_batch_host(const void* p_host, int64_t np, const void* q_host, int64_t nq,
+                   const int64_t* offsets_host, const int32_t* lengths_host, int64_t num_pairs,
+                   int32_t dim, int32_t norm, int32_t dtype, void* out_host, ffd_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * ffd_cdist — all-pairs distances between two dense curve sets (one shard).
+ *   out[(a - row_begin)*ld_out + b] = δ_dF(A_a, B_b)  for a ∈ [row_begin, row_end),
+ *   b ∈ [0, nB).  setA: [nA, lenA, dim], setB: [nB, lenB, dim] dense row-major.
+ *   out: float (FFD_F32) or int64 (FFD_I32), ld_out ≥ nB elements.
+ *   [row_begin, row_end) is the caller's shard (one rank's block of rows).
+ *   workspace: ≥ ffd_cdist_workspace_bytes() bytes (may be NULL if that is 0).
+ * ------------------------------------------------------------------------- */
+int ffd_cdist(const void* setA, int64_t nA, int32_t lenA, const void* setB, int64_t nB,
+              int32_t lenB, int32_t dim, int32_t norm, int32_t dtype, int64_t row_begin,
+              int64_t row_end, void* out, int64_t ld_out, void* workspace,
+              size_t workspace_bytes, ffd_stream_t stream);
+size_t ffd_cdist_workspace_bytes(void);
+
+/* ---------------------------------------------------------------------------
+ * ffd_validate_batch — SYNCHRONOUS device-data precondition check of a batch:
+ *   lengths ≥ 1 (FFD_ERR_EMPTY), offsets+lengths within [0, np)/[0, nq)
+ *   (FFD_ERR_RANGE), finite fp32 coordinates (FFD_ERR_NONFINITE), and for int32
+ *   input D·(max |coordinate difference within a pair|)² ≤ 2^63−1
+ *   (FFD_ERR_OVERFLOW).  Returns the first violated code in that order, FFD_OK
+ *   otherwise.  Uses no caller workspace.
+ * ------------------------------------------------------------------------- */
+int ffd_validate_batch(const void* p, int64_t np, const void* q, int64_t nq,
+                       const int64_t* offsets, const int32_t* lengths, int64_t num_pairs,
+                       int32_t dim, int32_t dtype, ffd_stream_t stream);
+
+/* human-readable name of a status code (static storage) */
+const char* ffd_status_string(int status);
+
+/* number of kernels the library launched on this thread since the last call
+ * (for launch accounting in benchmarks); resets the counter. */
+int64_t ffd_take_launch_count(void);
+
+/* library version: major*10000 + minor*100 + patch */
+int ffd_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FFD_H */

@@ -1,0 +1,190 @@
+"""B200-native discrete Fréchet distance (arxiv 2404.05708) — Python binding.
+
+Thin ctypes marshalling over the C ABI of include/ffd.h (libffd.so, built
+in-tree by ``python -m paper_2404_05708_b200.build``).  Every step of the
+computation runs in the library's CUDA kernels; PyTorch only provides device
+memory and streams.  There is no CPU fallback: if the library or a GPU is
+missing, calls raise.
+
+    batch(p, q, offsets, lengths, norm)        -> Tensor[B]   (ffd_batch)
+    batch_host(p, q, offsets, lengths, norm)   -> ndarray[B]  (ffd_batch_host)
+    cdist(A, B, norm, rows=None)               -> Tensor      (ffd_cdist)
+    validate(p, q, offsets, lengths)           -> status      (ffd_validate_batch)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libffd.so")
+
+L1, L2, LINF, SQL2 = 1, 2, 3, 4
+NORMS = {"l1": L1, "l2": L2, "linf": LINF, "sql2": SQL2}
+F32, I32 = 0, 1
+
+STATUS = {0: "ok", -1: "invalid argument", -2: "unsupported", -3: "CUDA error", -4: "empty curve",
+          -5: "non-finite coordinate", -6: "integer overflow", -7: "out of range",
+          -8: "workspace too small"}
+
+
+class FFDError(RuntimeError):
+    def __init__(self, status: int, what: str = ""):
+        super().__init__(f"{what}: ffd status {status} ({STATUS.get(status, '?')})")
+        self.status = status
+
+
+_lib = None
+
+
+def lib():
+    """Load libffd.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built; run `python -m paper_2404_05708_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I64, I32_, SZ = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_size_t
+        L.ffd_batch.argtypes = [P, P, P, P, I64, I32_, I32_, I32_, P, P, SZ, P]
+        L.ffd_batch.restype = ctypes.c_int
+        L.ffd_batch_workspace_bytes.argtypes = [I64]
+        L.ffd_batch_workspace_bytes.restype = SZ
+        L.ffd_batch_host.argtypes = [P, I64, P, I64, P, P, I64, I32_, I32_, I32_, P, P]
+        L.ffd_batch_host.restype = ctypes.c_int
+        L.ffd_cdist.argtypes = [P, I64, I32_, P, I64, I32_, I32_, I32_, I32_, I64, I64, P, I64, P, SZ, P]
+        L.ffd_cdist.restype = ctypes.c_int
+        L.ffd_cdist_workspace_bytes.argtypes = []
+        L.ffd_cdist_workspace_bytes.restype = SZ
+        L.ffd_validate_batch.argtypes = [P, I64, P, I64, P, P, I64, I32_, I32_, P]
+        L.ffd_validate_batch.restype = ctypes.c_int
+        L.ffd_status_string.argtypes = [ctypes.c_int]
+        L.ffd_status_string.restype = ctypes.c_char_p
+        L.ffd_take_launch_count.argtypes = []
+        L.ffd_take_launch_count.restype = I64
+        L.ffd_version.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+EXPORTED = ["ffd_batch", "ffd_batch_workspace_bytes", "ffd_batch_host", "ffd_cdist",
+            "ffd_cdist_workspace_bytes", "ffd_validate_batch", "ffd_status_string",
+            "ffd_take_launch_count", "ffd_version"]
+
+
+def _norm(norm) -> int:
+    return NORMS[norm] if isinstance(norm, str) else int(norm)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_ptr(stream):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dtype_code(t) -> int:
+    torch = _torch()
+    if t.dtype == torch.float32:
+        return F32
+    if t.dtype == torch.int32:
+        return I32
+    raise TypeError(f"coordinates must be float32 or int32, got {t.dtype}")
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        raise FFDError(status, what)
+
+
+_ws_cache: dict = {}
+
+
+def workspace(nbytes: int, device):
+    """Cached device workspace (grows on demand) per device."""
+    torch = _torch()
+    key = torch.device(device).index
+    buf = _ws_cache.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+        _ws_cache[key] = buf
+    return buf
+
+
+def launches_taken() -> int:
+    """Kernels the library launched on this thread since the previous call."""
+    return int(lib().ffd_take_launch_count())
+
+
+def batch(p, q, offsets, lengths, norm="l2", out=None, stream=None):
+    """δ_dF for B pairs (ffd_batch).  p [Σn, dim], q [Σm, dim] float32/int32 CUDA
+    tensors; offsets int64[2B]; lengths int32[2B].  Returns float32[B] (fp32
+    input) or int64[B] (int32 input)."""
+    torch = _torch()
+    if not (p.is_cuda and q.is_cuda and offsets.is_cuda and lengths.is_cuda):
+        raise ValueError("batch() takes CUDA tensors; use batch_host() for host arrays")
+    dt = _dtype_code(p)
+    if q.dtype != p.dtype or offsets.dtype != torch.int64 or lengths.dtype != torch.int32:
+        raise TypeError("dtype mismatch (p/q same dtype, offsets int64, lengths int32)")
+    p, q = p.contiguous(), q.contiguous()
+    B = offsets.numel() // 2
+    dim = p.shape[1]
+    if out is None:
+        out = torch.empty(B, dtype=torch.int64 if dt == I32 else torch.float32, device=p.device)
+    ws_bytes = lib().ffd_batch_workspace_bytes(B)
+    ws = workspace(ws_bytes, p.device)
+    _check(lib().ffd_batch(p.data_ptr(), q.data_ptr(), offsets.data_ptr(), lengths.data_ptr(), B, dim,
+                           _norm(norm), dt, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)),
+           "ffd_batch")
+    return out
+
+
+def batch_host(p: np.ndarray, q: np.ndarray, offsets: np.ndarray, lengths: np.ndarray, norm="l2",
+               out: np.ndarray | None = None, stream=None) -> np.ndarray:
+    """ffd_batch_host: host buffers in and out (copies inside the call)."""
+    p = np.ascontiguousarray(p)
+    q = np.ascontiguousarray(q)
+    offsets = np.ascontiguousarray(offsets, np.int64)
+    lengths = np.ascontiguousarray(lengths, np.int32)
+    dt = I32 if p.dtype == np.int32 else F32
+    B = offsets.shape[0] // 2
+    if out is None:
+        out = np.empty(B, np.int64 if dt == I32 else np.float32)
+    _check(lib().ffd_batch_host(p.ctypes.data, p.shape[0], q.ctypes.data, q.shape[0], offsets.ctypes.data,
+                                lengths.ctypes.data, B, p.shape[1], _norm(norm), dt, out.ctypes.data,
+                                _stream_ptr(stream)), "ffd_batch_host")
+    return out
+
+
+def cdist(A, B, norm="l2", rows=None, out=None, ld_out=None, stream=None):
+    """ffd_cdist on one shard: rows = (row_begin, row_end) of A (default all).
+    A [nA, lenA, dim], B [nB, lenB, dim] CUDA tensors.  Returns the block
+    [row_end-row_begin, nB] (float32, or int64 for int32 input)."""
+    torch = _torch()
+    dt = _dtype_code(A)
+    A, B = A.contiguous(), B.contiguous()
+    nA, lenA, dim = A.shape
+    nB, lenB, _ = B.shape
+    r0, r1 = (0, nA) if rows is None else rows
+    ld = nB if ld_out is None else ld_out
+    if out is None:
+        out = torch.empty((r1 - r0, ld), dtype=torch.int64 if dt == I32 else torch.float32, device=A.device)
+    wsb = lib().ffd_cdist_workspace_bytes()
+    ws = workspace(wsb, A.device) if wsb else None
+    _check(lib().ffd_cdist(A.data_ptr(), nA, lenA, B.data_ptr(), nB, lenB, dim, _norm(norm), dt, r0, r1,
+                           out.data_ptr(), ld, ws.data_ptr() if ws is not None else None, wsb,
+                           _stream_ptr(stream)), "ffd_cdist")
+    return out
+
+
+def validate(p, q, offsets, lengths, stream=None) -> int:
+    """ffd_validate_batch (synchronous); returns the status code."""
+    dt = _dtype_code(p)
+    B = offsets.numel() // 2
+    return int(lib().ffd_validate_batch(p.data_ptr(), p.shape[0], q.data_ptr(), q.shape[0], offsets.data_ptr(),
+                                        lengths.data_ptr(), B, p.shape[1], dt, _stream_ptr(stream)))

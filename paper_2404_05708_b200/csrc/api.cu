@@ -1,0 +1,321 @@
+// api.cu — the C ABI of include/ffd.h: argument checks, workspace layout,
+// dispatch to the compiled kernel instantiations, stream-ordered launches.
+#include <atomic>
+#include <climits>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "cdist.cuh"
+#include "ffd.h"
+#include "longpair.cuh"
+#include "prep.cuh"
+#include "registry.h"
+#include "strip.cuh"
+#include "validate.cuh"
+
+namespace ffd {
+
+// ---- registry -------------------------------------------------------------
+static std::vector<BatchEntry>& registry() {
+  static std::vector<BatchEntry> r;
+  return r;
+}
+static std::mutex& reg_mutex() {
+  static std::mutex m;
+  return m;
+}
+void register_batch(const BatchEntry& e) {
+  std::lock_guard<std::mutex> g(reg_mutex());
+  registry().push_back(e);
+}
+const BatchEntry* find_batch(const BatchKey& k) {
+  std::lock_guard<std::mutex> g(reg_mutex());
+  for (auto& e : registry())
+    if (e.key.tier == k.tier && e.key.kind == k.kind && e.key.dim == k.dim &&
+        e.key.int_in == k.int_in && e.key.fin == k.fin)
+      return &e;
+  return nullptr;
+}
+
+// ---- device facts -----------------------------------------------------------
+struct DevInfo {
+  int sms = 0;
+};
+static DevInfo dev_info() {
+  static DevInfo cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return DevInfo{148};
+  if (cache[dev].sms == 0) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev].sms = sms;
+  }
+  return cache[dev];
+}
+
+static thread_local int64_t g_launches = 0;
+
+constexpr int kMaxCtasMain = 6;  // cap on resident CTAs/SM used to size scratch
+constexpr int kCtasFb = 1;
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// workspace layout for a batch of B pairs on a device with `sms` SMs
+static BatchWs batch_layout(void* base, int64_t B, int sms) {
+  BatchWs w{};
+  size_t off = 0;
+  char* b = reinterpret_cast<char*>(base);
+  auto take = [&](size_t bytes) {
+    char* p = b ? b + off : nullptr;
+    off = align_up(off + bytes, 256);
+    return p;
+  };
+  w.counters = reinterpret_cast<int*>(take(sizeof(int) * kNumCtr));
+  w.hist = reinterpret_cast<int*>(take(sizeof(int) * kNumKeys));
+  w.cursor = reinterpret_cast<int*>(take(sizeof(int) * kNumKeys));
+  w.tmp = reinterpret_cast<PairDesc*>(take(sizeof(PairDesc) * (size_t)B));
+  w.sorted = reinterpret_cast<PairDesc*>(take(sizeof(PairDesc) * (size_t)B));
+  w.keys = reinterpret_cast<int16_t*>(take(sizeof(int16_t) * (size_t)B));
+  w.fb_list = reinterpret_cast<int*>(take(sizeof(int) * (size_t)B));
+  w.long_list = reinterpret_cast<int*>(take(sizeof(int) * (size_t)B));
+  const size_t warps_main = (size_t)sms * kMaxCtasMain * kWarpsPerCta;
+  const size_t warps_fb = (size_t)sms * kCtasFb * kWarpsPerCta;
+  w.scratch_main = reinterpret_cast<float*>(take(warps_main * 2 * kScratchCols * sizeof(float)));
+  w.scratch_fb = reinterpret_cast<long long*>(take(warps_fb * 2 * kScratchCols * sizeof(long long)));
+  w.bytes = off;
+  return w;
+}
+
+static int kind_for(int norm, int dtype) {
+  if (dtype == FFD_I32) return norm == FFD_SQL2 ? K_XSQ : (norm == FFD_L1 ? K_L1 : K_LINF);
+  return norm == FFD_L1 ? K_L1 : (norm == FFD_LINF ? K_LINF : K_SQ);
+}
+
+static int check_common(int32_t dim, int32_t norm, int32_t dtype) {
+  if (dim < 1 || dim > 4) return FFD_ERR_ARG;
+  if (norm < FFD_L1 || norm > FFD_SQL2) return FFD_ERR_ARG;
+  if (dtype != FFD_F32 && dtype != FFD_I32) return FFD_ERR_ARG;
+  if (dtype == FFD_I32 && norm == FFD_L2) return FFD_ERR_ARG;
+  return FFD_OK;
+}
+
+static int batch_impl(const void* p, const void* q, const int64_t* offsets, const int32_t* lengths,
+                      int64_t B, int32_t dim, int32_t norm, int32_t dtype, void* out,
+                      void* workspace, size_t ws_bytes, cudaStream_t st) {
+  int s = check_common(dim, norm, dtype);
+  if (s) return s;
+  if (B < 0) return FFD_ERR_ARG;
+  if (B == 0) return FFD_OK;
+  if (!p || !q || !offsets || !lengths || !out) return FFD_ERR_ARG;
+  if (B > INT_MAX / 2) return FFD_ERR_UNSUPPORTED;
+  const DevInfo di = dev_info();
+  BatchWs ws = batch_layout(workspace, B, di.sms);
+  if (!workspace || ws_bytes < ws.bytes) return FFD_ERR_WORKSPACE;
+
+  const int int_in = dtype == FFD_I32;
+  const int kind = kind_for(norm, dtype);
+  const int fin = (norm == FFD_L2) ? F_SQRT : F_NONE;
+  const BatchEntry* main_e = find_batch(BatchKey{0, kind, dim, int_in, fin});
+  if (!main_e) return FFD_ERR_UNSUPPORTED;
+  const BatchEntry* fb_e = nullptr;
+  if (int_in) {
+    const int fkind = norm == FFD_SQL2 ? K_SQ : (norm == FFD_L1 ? K_L1 : K_LINF);
+    fb_e = find_batch(BatchKey{1, fkind, dim, 1, F_NONE});
+    if (!fb_e) return FFD_ERR_UNSUPPORTED;
+  }
+
+  // zero counters + histogram (one memset of the leading block)
+  if (cudaMemsetAsync(ws.counters, 0,
+                      reinterpret_cast<char*>(ws.cursor) - reinterpret_cast<char*>(ws.counters),
+                      st) != cudaSuccess)
+    return FFD_ERR_CUDA;
+  if (launch_prep(offsets, lengths, B, int_in, out, ws, di.sms, st, &g_launches) != cudaSuccess)
+    return FFD_ERR_CUDA;
+
+  Problem pb{};
+  pb.p = p;
+  pb.q = q;
+  pb.offsets = offsets;
+  pb.lengths = lengths;
+  pb.num_pairs = B;
+  pb.sorted = ws.sorted;
+  pb.num_sorted = ws.counters + kCtrNumSorted;
+  pb.counter = ws.counters + kCtrChunkMain;
+  pb.out = out;
+  pb.scratch = ws.scratch_main;
+  pb.fb_list = ws.fb_list;
+  pb.fb_count = ws.counters + kCtrFb;
+  std::memcpy(pb.rmap, main_e->rmap, sizeof(pb.rmap));
+  int occ = main_e->occupancy();
+  if (occ < 1) occ = 1;
+  if (occ > kMaxCtasMain) occ = kMaxCtasMain;
+  if (main_e->launch(pb, di.sms * occ, st) != cudaSuccess) return FFD_ERR_CUDA;
+  ++g_launches;
+
+  if (fb_e) {
+    Problem fb = pb;
+    fb.list = ws.fb_list;
+    fb.list_count = ws.counters + kCtrFb;
+    fb.counter = ws.counters + kCtrChunkFb;
+    fb.scratch = reinterpret_cast<float*>(ws.scratch_fb);
+    fb.fb_list = nullptr;
+    fb.fb_count = nullptr;
+    std::memcpy(fb.rmap, fb_e->rmap, sizeof(fb.rmap));
+    if (fb_e->launch(fb, di.sms * kCtasFb, st) != cudaSuccess) return FFD_ERR_CUDA;
+    ++g_launches;
+  }
+
+  // pairs too long for the band scratch of the batch kernel: cross-CTA wavefront
+  LongArgs la{};
+  la.p = p;
+  la.q = q;
+  la.offsets = offsets;
+  la.lengths = lengths;
+  la.num_pairs = B;
+  la.dim = dim;
+  la.norm = norm;
+  la.dtype = dtype;
+  la.list = ws.long_list;
+  la.list_count = ws.counters + kCtrLong;
+  la.out = out;
+  if (launch_long_pairs(la, di.sms, st, &g_launches) != cudaSuccess) return FFD_ERR_CUDA;
+  return FFD_OK;
+}
+
+}  // namespace ffd
+
+using namespace ffd;
+
+extern "C" {
+
+int ffd_version(void) { return 100; }
+
+const char* ffd_status_string(int s) {
+  switch (s) {
+    case FFD_OK: return "ok";
+    case FFD_ERR_ARG: return "invalid argument";
+    case FFD_ERR_UNSUPPORTED: return "unsupported";
+    case FFD_ERR_CUDA: return "CUDA error";
+    case FFD_ERR_EMPTY: return "curve with length < 1";
+    case FFD_ERR_NONFINITE: return "non-finite coordinate";
+    case FFD_ERR_OVERFLOW: return "integer distance overflows int64";
+    case FFD_ERR_RANGE: return "offsets/lengths out of range";
+    case FFD_ERR_WORKSPACE: return "workspace too small";
+    default: return "unknown status";
+  }
+}
+
+int64_t ffd_take_launch_count(void) {
+  int64_t n = g_launches;
+  g_launches = 0;
+  return n;
+}
+
+size_t ffd_batch_workspace_bytes(int64_t num_pairs) {
+  if (num_pairs < 0) return 0;
+  return batch_layout(nullptr, num_pairs, dev_info().sms).bytes;
+}
+
+int ffd_batch(const void* p, const void* q, const int64_t* offsets, const int32_t* lengths,
+              int64_t num_pairs, int32_t dim, int32_t norm, int32_t dtype, void* out,
+              void* workspace, size_t workspace_bytes, ffd_stream_t stream) {
+  return batch_impl(p, q, offsets, lengths, num_pairs, dim, norm, dtype, out, workspace,
+                    workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ffd_batch_host(const void* p_host, int64_t np, const void* q_host, int64_t nq,
+                   const int64_t* offsets_host, const int32_t* lengths_host, int64_t num_pairs,
+                   int32_t dim, int32_t norm, int32_t dtype, void* out_host, ffd_stream_t stream) {
+  int s = check_common(dim, norm, dtype);
+  if (s) return s;
+  if (num_pairs < 0 || np < 0 || nq < 0) return FFD_ERR_ARG;
+  if (num_pairs == 0) return FFD_OK;
+  if (!p_host || !q_host || !offsets_host || !lengths_host || !out_host) return FFD_ERR_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  static std::once_flag pool_once;
+  std::call_once(pool_once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+  const size_t esz = 4;
+  const size_t pb = (size_t)np * dim * esz, qb = (size_t)nq * dim * esz;
+  const size_t ob = (size_t)num_pairs * (dtype == FFD_I32 ? 8 : 4);
+  const size_t offb = (size_t)num_pairs * 2 * sizeof(int64_t);
+  const size_t lenb = (size_t)num_pairs * 2 * sizeof(int32_t);
+  const size_t wsb = ffd_batch_workspace_bytes(num_pairs);
+  void *dp = nullptr, *dq = nullptr, *doff = nullptr, *dlen = nullptr, *dout = nullptr, *dws = nullptr;
+  int rc = FFD_OK;
+  if (cudaMallocAsync(&dp, pb ? pb : 16, st) || cudaMallocAsync(&dq, qb ? qb : 16, st) ||
+      cudaMallocAsync(&doff, offb, st) || cudaMallocAsync(&dlen, lenb, st) ||
+      cudaMallocAsync(&dout, ob, st) || cudaMallocAsync(&dws, wsb, st)) {
+    rc = FFD_ERR_CUDA;
+  }
+  if (rc == FFD_OK) {
+    if (cudaMemcpyAsync(dp, p_host, pb, cudaMemcpyHostToDevice, st) ||
+        cudaMemcpyAsync(dq, q_host, qb, cudaMemcpyHostToDevice, st) ||
+        cudaMemcpyAsync(doff, offsets_host, offb, cudaMemcpyHostToDevice, st) ||
+        cudaMemcpyAsync(dlen, lengths_host, lenb, cudaMemcpyHostToDevice, st))
+      rc = FFD_ERR_CUDA;
+  }
+  if (rc == FFD_OK)
+    rc = batch_impl(dp, dq, reinterpret_cast<int64_t*>(doff), reinterpret_cast<int32_t*>(dlen),
+                    num_pairs, dim, norm, dtype, dout, dws, wsb, st);
+  if (rc == FFD_OK && cudaMemcpyAsync(out_host, dout, ob, cudaMemcpyDeviceToHost, st))
+    rc = FFD_ERR_CUDA;
+  for (void* ptr : {dp, dq, doff, dlen, dout, dws})
+    if (ptr) cudaFreeAsync(ptr, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess && rc == FFD_OK) rc = FFD_ERR_CUDA;
+  return rc;
+}
+
+size_t ffd_cdist_workspace_bytes(void) { return cdist_workspace_bytes(); }
+
+int ffd_cdist(const void* setA, int64_t nA, int32_t lenA, const void* setB, int64_t nB,
+              int32_t lenB, int32_t dim, int32_t norm, int32_t dtype, int64_t row_begin,
+              int64_t row_end, void* out, int64_t ld_out, void* workspace, size_t workspace_bytes,
+              ffd_stream_t stream) {
+  int s = check_common(dim, norm, dtype);
+  if (s) return s;
+  if (nA < 0 || nB < 0 || row_begin < 0 || row_end < row_begin || row_end > nA) return FFD_ERR_ARG;
+  if (ld_out < nB) return FFD_ERR_ARG;
+  if (row_end == row_begin || nB == 0) return FFD_OK;
+  if (!setA || !setB || !out || lenA < 1 || lenB < 1) return FFD_ERR_ARG;
+  if (workspace_bytes < cdist_workspace_bytes() || (!workspace && cdist_workspace_bytes() > 0))
+    return FFD_ERR_WORKSPACE;
+  CdistArgs a{};
+  a.A = setA;
+  a.B = setB;
+  a.nA = nA;
+  a.nB = nB;
+  a.lenA = lenA;
+  a.lenB = lenB;
+  a.dim = dim;
+  a.norm = norm;
+  a.dtype = dtype;
+  a.row_begin = row_begin;
+  a.row_end = row_end;
+  a.out = out;
+  a.ld_out = ld_out;
+  a.workspace = workspace;
+  return launch_cdist(a, dev_info().sms, reinterpret_cast<cudaStream_t>(stream), &g_launches);
+}
+
+int ffd_validate_batch(const void* p, int64_t np, const void* q, int64_t nq,
+                       const int64_t* offsets, const int32_t* lengths, int64_t num_pairs,
+                       int32_t dim, int32_t dtype, ffd_stream_t stream) {
+  if (dim < 1 || dim > 4 || (dtype != FFD_F32 && dtype != FFD_I32) || num_pairs < 0 || np < 0 ||
+      nq < 0)
+    return FFD_ERR_ARG;
+  if (num_pairs == 0) return FFD_OK;
+  if (!offsets || !lengths || (np > 0 && !p) || (nq > 0 && !q)) return FFD_ERR_ARG;
+  return validate_batch(p, np, q, nq, offsets, lengths, num_pairs, dim, dtype,
+                        reinterpret_cast<cudaStream_t>(stream), &g_launches);
+}
+
+}  // extern "C"

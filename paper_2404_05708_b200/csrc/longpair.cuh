@@ -1,0 +1,19 @@
+// longpair.cuh — pairs too long for the batch kernel's band scratch.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ffd {
+struct LongArgs {
+  const void* p;
+  const void* q;
+  const int64_t* offsets;
+  const int32_t* lengths;
+  int64_t num_pairs;
+  int dim, norm, dtype;
+  const int* list;        // device list of long pair indices
+  const int* list_count;  // device count
+  void* out;
+};
+cudaError_t launch_long_pairs(const LongArgs& a, int sms, cudaStream_t st, int64_t* launches);
+}  // namespace ffd

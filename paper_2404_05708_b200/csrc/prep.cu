@@ -1,0 +1,104 @@
+// prep.cu — per-call preparation of a batch: band shape of every pair and a
+// counting sort of the pairs by shape, longest first ("sorting
+// the curves by their respective lengths before assigning them to batches").
+//
+// key = (nb − 1)·16 + (R − 1) where the pair's rows curve (the shorter one; δ is
+// symmetric) is covered by nb bands of 32·R rows, R ≤ 16.  Pairs with a length
+// < 1 get their invalid-output value here and are dropped; pairs too long for
+// the batch kernel's band scratch go to the long-pair list.
+#include "prep.cuh"
+
+namespace ffd {
+
+__global__ void prep_keys_kernel(const int64_t* __restrict__ offsets,
+                                 const int32_t* __restrict__ lengths, int64_t B, int int_out,
+                                 void* __restrict__ out, PairDesc* __restrict__ tmp,
+                                 int16_t* __restrict__ keys, int* __restrict__ hist,
+                                 int* __restrict__ long_list, int* __restrict__ long_count) {
+  __shared__ int h[kNumKeys];
+  for (int i = threadIdx.x; i < kNumKeys; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < B;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int n = lengths[k], m = lengths[B + k];
+    int key = -1;
+    if (n < 1 || m < 1) {
+      if (int_out) reinterpret_cast<long long*>(out)[k] = LLONG_MIN;
+      else reinterpret_cast<float*>(out)[k] = __int_as_float(0x7fc00000);
+    } else {
+      const bool swap = n > m;
+      const int rows = swap ? m : n, cols = swap ? n : m;
+      const int nb = (rows + kWarp * kMaxR - 1) / (kWarp * kMaxR);
+      if (nb > kMaxBands || (nb > 1 && cols + 2 > kScratchCols)) {
+        long_list[atomicAdd(long_count, 1)] = (int)k;
+      } else {
+        const int R = (rows + kWarp * nb - 1) / (kWarp * nb);
+        PairDesc d;
+        d.row_off = swap ? offsets[B + k] : offsets[k];
+        d.col_off = swap ? offsets[k] : offsets[B + k];
+        d.n_rows = rows;
+        d.m_cols = cols;
+        d.idx = (int)k;
+        d.R = (uint8_t)R;
+        d.nb = (uint8_t)nb;
+        d.swap = swap;
+        d.pad = 0;
+        tmp[k] = d;
+        key = (nb - 1) * kMaxR + (R - 1);
+        atomicAdd(&h[key], 1);
+      }
+    }
+    keys[k] = (int16_t)key;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kNumKeys; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+// one block of kNumKeys threads: descending-key exclusive scan -> bin cursors
+__global__ void prep_scan_kernel(const int* __restrict__ hist, int* __restrict__ cursor,
+                                 int* __restrict__ num_sorted) {
+  __shared__ int s[kNumKeys];
+  const int i = threadIdx.x;
+  // position in descending order: bin i gets Σ_{j > i} hist[j]
+  s[i] = hist[kNumKeys - 1 - i];
+  __syncthreads();
+  for (int o = 1; o < kNumKeys; o <<= 1) {
+    int v = (i >= o) ? s[i - o] : 0;
+    __syncthreads();
+    s[i] += v;
+    __syncthreads();
+  }
+  // s[i] = inclusive sum over reversed bins 0..i  ->  exclusive for bin (K-1-i)
+  const int bin = kNumKeys - 1 - i;
+  cursor[bin] = s[i] - hist[bin];
+  if (i == kNumKeys - 1) *num_sorted = s[i];
+}
+
+__global__ void prep_scatter_kernel(const PairDesc* __restrict__ tmp,
+                                    const int16_t* __restrict__ keys, int64_t B,
+                                    int* __restrict__ cursor, PairDesc* __restrict__ sorted) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < B;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int key = keys[k];
+    if (key >= 0) sorted[atomicAdd(&cursor[key], 1)] = tmp[k];
+  }
+}
+
+cudaError_t launch_prep(const int64_t* offsets, const int32_t* lengths, int64_t B, int int_out,
+                        void* out, const BatchWs& ws, int num_sms, cudaStream_t st,
+                        int64_t* launches) {
+  if (B == 0) return cudaSuccess;
+  const int threads = 256;
+  int64_t blocks = (B + threads - 1) / threads;
+  if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
+  prep_keys_kernel<<<(int)blocks, threads, 0, st>>>(offsets, lengths, B, int_out, out, ws.tmp,
+                                                    ws.keys, ws.hist, ws.long_list,
+                                                    ws.counters + kCtrLong);
+  prep_scan_kernel<<<1, kNumKeys, 0, st>>>(ws.hist, ws.cursor, ws.counters + kCtrNumSorted);
+  prep_scatter_kernel<<<(int)blocks, threads, 0, st>>>(ws.tmp, ws.keys, B, ws.cursor, ws.sorted);
+  *launches += 3;
+  return cudaGetLastError();
+}
+
+}  // namespace ffd

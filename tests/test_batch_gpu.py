@@ -1,0 +1,154 @@
+"""Parity of ffd_batch (CUDA, through the C ABI) against the CPU oracle.
+
+Integer inputs: bit-exact against the exact int64 oracle.  fp32 inputs: within
+1e-5 relative of the fp64 oracle (BASELINE.json north_star) AND bit-exact
+against the oracle's fp32 mirror.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workload
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def ffd():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2404_05708_b200 as ffd
+    ffd.lib()
+    return ffd
+
+
+def to_dev(b: workload.Batch):
+    d = "cuda"
+    return (torch.from_numpy(b.p).to(d), torch.from_numpy(b.q).to(d),
+            torch.from_numpy(b.offsets).to(d), torch.from_numpy(b.lengths).to(d))
+
+
+def check_float(got, b, norm, threads=0):
+    ref = oracle.batch(b.p, b.q, b.offsets, b.lengths, b.dim, norm, threads=threads)
+    mir = oracle.batch(b.p, b.q, b.offsets, b.lengths, b.dim, norm, threads=threads, mirror=True)
+    got = np.asarray(got)
+    err = np.abs(got.astype(np.float64) - ref)
+    bad = err > TOL * np.abs(ref)
+    assert not bad.any(), f"{bad.sum()} pairs beyond 1e-5 rel; first {np.nonzero(bad)[0][:5]} got {got[bad][:5]} ref {ref[bad][:5]}"
+    mism = got != mir
+    assert not mism.any(), f"{mism.sum()} pairs differ from the fp32 mirror; first {np.nonzero(mism)[0][:5]}"
+
+
+def check_int(got, b, norm, threads=0):
+    ref = oracle.batch(b.p, b.q, b.offsets, b.lengths, b.dim, norm, threads=threads)
+    got = np.asarray(got)
+    mism = got != ref
+    assert not mism.any(), f"{mism.sum()} mismatches; first {np.nonzero(mism)[0][:5]} got {got[mism][:5]} ref {ref[mism][:5]}"
+
+
+def make_batch(rng, B, lo, hi, dim=2, kind="f", scale=1.0, lens=None):
+    if lens is None:
+        lens = rng.integers(lo, hi + 1, size=2 * B).astype(np.int32)
+    off = np.zeros(2 * B, np.int64)
+    np_, nq = int(lens[:B].sum()), int(lens[B:].sum())
+    off[1:B] = np.cumsum(lens[:B - 1])
+    off[B + 1:] = np.cumsum(lens[B:-1])
+    if kind == "i":
+        p = np.cumsum(rng.integers(-8, 9, size=(np_, dim)), axis=0).astype(np.int32)
+        q = np.cumsum(rng.integers(-8, 9, size=(nq, dim)), axis=0).astype(np.int32)
+        p = (p * scale).astype(np.int32)
+        q = (q * scale).astype(np.int32)
+    else:
+        p = (np.cumsum(rng.normal(size=(np_, dim)), axis=0) * scale).astype(np.float32)
+        q = (np.cumsum(rng.normal(size=(nq, dim)), axis=0) * scale).astype(np.float32)
+    return workload.Batch(p, q, off, lens, dim, "l2")
+
+
+def test_config1_full(ffd):
+    b = workload.gen_batch(workload.CONFIGS[1])
+    out = ffd.batch(*to_dev(b), norm="l2")
+    check_float(out.cpu().numpy(), b, "l2")
+
+
+@pytest.mark.parametrize("lo,hi", [(1, 40), (30, 130), (100, 520), (500, 1100)])
+def test_random_lengths_f32_l2(ffd, lo, hi):
+    rng = np.random.default_rng(lo * 7 + hi)
+    b = make_batch(rng, 300, lo, hi)
+    out = ffd.batch(*to_dev(b), norm="l2")
+    check_float(out.cpu().numpy(), b, "l2")
+
+
+def test_config2_subset_exact(ffd):
+    cfg = workload.CONFIGS[2].scaled(pairs=4000)
+    b = workload.gen_batch(cfg)
+    out = ffd.batch(*to_dev(b), norm="sql2")
+    check_int(out.cpu().numpy(), b, "sql2")
+
+
+@pytest.mark.parametrize("lo,hi", [(1, 40), (100, 600), (480, 1100)])
+def test_random_int_exact(ffd, lo, hi):
+    rng = np.random.default_rng(lo + hi)
+    b = make_batch(rng, 300, lo, hi, kind="i")
+    out = ffd.batch(*to_dev(b), norm="sql2")
+    check_int(out.cpu().numpy(), b, "sql2")
+
+
+def test_int_outside_fp32_window_uses_exact_tier(ffd):
+    """coordinates far beyond ±1448 (the fp32-exact window) must stay exact."""
+    rng = np.random.default_rng(5)
+    b = make_batch(rng, 200, 1, 300, kind="i", scale=5000.0)
+    # mix: half the pairs in-window, half out
+    b.p[: b.p.shape[0] // 3] //= 5000
+    out = ffd.batch(*to_dev(b), norm="sql2")
+    check_int(out.cpu().numpy(), b, "sql2")
+
+
+def test_edge_lengths(ffd):
+    rng = np.random.default_rng(9)
+    lens = np.array([1, 1, 2, 64, 513, 1, 33, 32, 31, 600,
+                     1, 7, 1, 64, 1, 700, 32, 33, 31, 599], np.int32)
+    b = make_batch(rng, 10, 0, 0, lens=lens)
+    out = ffd.batch(*to_dev(b), norm="l2")
+    check_float(out.cpu().numpy(), b, "l2")
+
+
+def test_empty_pair_gets_nan(ffd):
+    rng = np.random.default_rng(10)
+    lens = np.array([5, 0, 6, 7, 3, 4], np.int32)
+    b = make_batch(rng, 3, 0, 0, lens=lens)
+    out = ffd.batch(*to_dev(b), norm="l2").cpu().numpy()
+    assert np.isnan(out[1])
+    ok = [0, 2]
+    for k in ok:
+        B = 3
+        pk = b.p[b.offsets[k]: b.offsets[k] + b.lengths[k]]
+        qk = b.q[b.offsets[B + k]: b.offsets[B + k] + b.lengths[B + k]]
+        assert out[k] == oracle.pair(pk, qk, "l2", form="mirror")
+
+
+def test_identity_and_symmetry(ffd):
+    rng = np.random.default_rng(11)
+    b = make_batch(rng, 100, 1, 400)
+    B = b.num_pairs
+    # q := p  -> δ = 0
+    same = workload.Batch(b.p, b.p, np.concatenate([b.offsets[:B], b.offsets[:B]]),
+                          np.concatenate([b.lengths[:B], b.lengths[:B]]), 2, "l2")
+    out = ffd.batch(*to_dev(same), norm="l2").cpu().numpy()
+    assert (out == 0).all()
+    # swap p and q -> identical bits
+    sw = workload.Batch(b.q, b.p, np.concatenate([b.offsets[B:], b.offsets[:B]]),
+                        np.concatenate([b.lengths[B:], b.lengths[:B]]), 2, "l2")
+    o1 = ffd.batch(*to_dev(b), norm="l2").cpu().numpy()
+    o2 = ffd.batch(*to_dev(sw), norm="l2").cpu().numpy()
+    assert np.array_equal(o1, o2)
+
+
+def test_batch_host_matches_device(ffd):
+    cfg = workload.CONFIGS[2].scaled(pairs=500)
+    b = workload.gen_batch(cfg)
+    dev = ffd.batch(*to_dev(b), norm="sql2").cpu().numpy()
+    host = ffd.batch_host(b.p, b.q, b.offsets, b.lengths, norm="sql2")
+    assert np.array_equal(dev, host)

@@ -1,0 +1,323 @@
+#!/usr/bin/env python
+"""Benchmark: DP cells/s of the discrete Fréchet hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ffd|reference]
+
+One "step" = one ffd_batch call over the whole config-2 batch (100k pairs,
+2-D int32, lengths U[128,512], squared L2, exact) with inputs resident in HBM
+(512 MB > 126 MB L2: no L2 flush needed).  Multi-GPU (torchrun, one rank per
+GPU): every rank processes its own 100k-pair shard (weak scaling, no data-path
+collective); time = max over ranks.  Rank 0 prints ONE JSON line.
+
+--impl reference times the CPU oracle (oracle/, the plain C table DP) on the
+host cores on a bounded sample of the same workload — the slow reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workload  # noqa: E402
+
+METRIC = "DP cells/sec (G cells/s) batched & all-pairs Fréchet; % of ALU roofline"
+UNIT = "Gcells/s"
+SM_MAX_MHZ_NOMINAL = 1965.0
+# ALU roofline: 148 SMs × 4 SMSPs × 32 lanes = 128 lane-ops/clk/SM of the
+# FP32/INT pipe; cells/s = 148·128·f / ops_per_cell, ops_per_cell = minimal SASS pipe-ops per cell.
+OPS_PER_CELL = {1: 7, 2: 6, 3: 9, 4: 7, 5: 7}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.samples = []
+        self.reasons = set()
+        self.period = period_s
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+            "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_sample(cfg, target_cells: float):
+    """First pairs of the workload totalling ≈ target_cells cells (bounded CPU sample)."""
+    lp = workload.gen_lengths(cfg, "p")
+    lq = workload.gen_lengths(cfg, "q")
+    cum = np.cumsum(lp.astype(np.int64) * lq.astype(np.int64))
+    k = int(np.searchsorted(cum, target_cells)) + 1
+    k = max(1, min(k, cfg.pairs))
+    return workload.gen_batch(cfg.scaled(pairs=k)), k
+
+
+def run_oracle_timed(b, cfg, threads):
+    import oracle
+    t0 = time.perf_counter()
+    oracle.batch(b.p, b.q, b.offsets, b.lengths, b.dim, cfg.norm, threads=threads)
+    return time.perf_counter() - t0
+
+
+def bench_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    cfg = workload.CONFIGS[args.config]
+    cores = cpu_cores()
+    b, k = oracle_sample(cfg, 3e8)
+    cells = b.cells()
+    for _ in range(args.warmup):
+        run_oracle_timed(b, cfg, cores)
+    t = sum(run_oracle_timed(b, cfg, cores) for _ in range(args.steps))
+    value = cells * args.steps / t / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic", "config": {"workload": cfg.name, "sample_pairs": k, "sample_cells": cells},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"first {k} pairs of {cfg.name} ({cells:.3g} cells) per step, "
+                                   f"plain C table DP, OpenMP over pairs"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def bench_ffd(args):
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local if ws > 1 else 0)
+    torch.cuda.set_device(dev)
+    import paper_2404_05708_b200 as ffd
+    ffd.lib()
+
+    cfg = workload.CONFIGS[args.config]
+    assert cfg.kind == "batch", "bench.py times the batch path (configs 1-3)"
+    first = rank * cfg.pairs
+
+    def pinned(shape, dtype):
+        t = torch.empty(shape, dtype=torch.from_numpy(np.zeros(0, dtype)).dtype, pin_memory=True)
+        return t.numpy()
+
+    b = workload.gen_batch(cfg, alloc=pinned, first=first)
+    cells = b.cells()
+    B = b.num_pairs
+    p = torch.from_numpy(b.p).to(dev)
+    q = torch.from_numpy(b.q).to(dev)
+    off_h = torch.from_numpy(b.offsets).pin_memory()
+    len_h = torch.from_numpy(b.lengths).pin_memory()
+    off = off_h.to(dev)
+    lens = len_h.to(dev)
+    out = torch.empty(B, dtype=torch.int64 if cfg.dtype == "i32" else torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if ws == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: float) -> float:
+        if ws == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    # ---- device-resident timing ------------------------------------------------
+    for _ in range(args.warmup):
+        ffd.batch(p, q, off, lens, norm=cfg.norm, out=out)
+    torch.cuda.synchronize()
+    ffd.launches_taken()
+    ffd.profile_take()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(dev.index)
+    ffd.profile_enable(True)
+    with sampler:
+        e0.record(stream)
+        for _ in range(args.steps):
+            ffd.batch(p, q, off, lens, norm=cfg.norm, out=out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ffd.profile_enable(False)
+    barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = ffd.launches_taken() // args.steps
+    kern_ms_total, kern_n = ffd.profile_take()
+    kern_ms = kern_ms_total / max(kern_n, 1)
+    checksum = int(out.sum().item()) if cfg.dtype == "i32" else float(out.double().sum().item())
+    ms_max = max_over_ranks(ms)
+    total_cells = sum_over_ranks(float(cells))
+    value = total_cells / (ms_max * 1e-3) / 1e9
+
+    # ---- end to end through the C ABI with host buffers (ffd_batch_host) -------
+    out_h = torch.empty(B, dtype=out.dtype, pin_memory=True).numpy()
+    for _ in range(max(1, min(args.warmup, 2))):
+        ffd.batch_host(b.p, b.q, b.offsets, b.lengths, norm=cfg.norm, out=out_h)
+    barrier()
+    torch.cuda.synchronize()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(args.steps):
+        ffd.batch_host(b.p, b.q, b.offsets, b.lengths, norm=cfg.norm, out=out_h)
+    e3.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = max_over_ranks(e2.elapsed_time(e3) / args.steps)
+    e2e_ok = bool(np.array_equal(out_h, out.cpu().numpy()))
+    h2d = b.p.nbytes + b.q.nbytes + b.offsets.nbytes + b.lengths.nbytes
+    d2h = out_h.nbytes
+
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return 0
+
+    clocks = sampler.summary()
+    f_meas = (clocks["sm_mhz"] or SM_MAX_MHZ_NOMINAL) * 1e6
+    f_max = (clocks["sm_max_mhz"] or SM_MAX_MHZ_NOMINAL) * 1e6
+    ops = OPS_PER_CELL[cfg.cid]
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak = sms * 128 * f_max / ops / 1e9
+    achieved = cells / (kern_ms * 1e-3) / 1e9
+    roofline = {
+        "bound": "alu", "achieved": achieved, "peak": peak, "unit": UNIT,
+        "frac": achieved / peak, "traffic": args.traffic,
+        "kernel": "batch_kernel (fp32-exact int sqL2 cell)", "kernel_ms": kern_ms,
+        "ops_per_cell": ops,
+        "peak_basis": f"{sms} SMs x 128 lane-ops/clk x {f_max/1e6:.0f} MHz (max clock) / {ops} ops per cell",
+        "frac_at_measured_clock": achieved / (sms * 128 * f_meas / ops / 1e9),
+    }
+
+    cpu = None
+    if ws == 1 and not args.no_cpu_baseline:
+        cores = cpu_cores()
+        sb, k = oracle_sample(cfg, args.cpu_cells)
+        t = run_oracle_timed(sb, cfg, cores)
+        cpu = {"value": sb.cells() / t / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"first {k} pairs of {cfg.name} ({sb.cells():.3g} cells), plain C table DP "
+                         f"(oracle/ffd_oracle.c), OpenMP over pairs, {t:.1f} s"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32" if cfg.dtype == "f32" else "f32-exact-int",
+        "data": "synthetic",
+        "config": {"workload": cfg.name, "pairs_per_gpu": B, "cells_per_gpu_step": cells,
+                   "dim": cfg.dim, "norm": cfg.norm, "lengths": list(cfg.len_p),
+                   "l2": "inputs larger than L2 (%.0f MB per GPU)" % ((b.p.nbytes + b.q.nbytes) / 1e6),
+                   "parallelism": f"pairs sharded over {ws} GPU(s), no collective on the data path"},
+        "clocks": clocks,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": {"value": total_cells / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "matches_device_result": e2e_ok,
+                "api": "ffd_batch_host (pinned host buffers, H2D + kernels + D2H per step)"},
+        "gpu_launches": launches * args.steps,
+        "gpu_launches_per_step": launches,
+        "checksum": checksum,
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ffd", choices=["ffd", "reference"])
+    ap.add_argument("--cpu-cells", type=float, default=3e9, help="cells in the oracle cpu_baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="dram bytes per launch of the dominant kernel from an ncu --set full capture")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return bench_reference(args)
+    return bench_ffd(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -114,6 +114,16 @@ int ffd_validate_batch(const void* p, int64_t np, const void* q, int64_t nq,
                        const int64_t* offsets, const int32_t* lengths, int64_t num_pairs,
                        int32_t dim, int32_t dtype, ffd_stream_t stream);
 
+/* ---------------------------------------------------------------------------
+ * Profiling hook (benchmarks): while enabled, every ffd_batch / ffd_cdist call
+ * records a CUDA event pair on its stream around its dominant kernel (the
+ * batch / cdist / long-pair DP kernel).  ffd_profile_take() waits for the
+ * recorded events, writes the summed kernel milliseconds and the number of
+ * timed launches, and clears the record.  Host-side, thread-safe.
+ * ------------------------------------------------------------------------- */
+int ffd_profile_enable(int on);
+int ffd_profile_take(double* total_ms, int64_t* launches);
+
 /* human-readable name of a status code (static storage) */
 const char* ffd_status_string(int status);
 

@@ -64,13 +64,17 @@ def lib():
         L.ffd_take_launch_count.argtypes = []
         L.ffd_take_launch_count.restype = I64
         L.ffd_version.restype = ctypes.c_int
+        L.ffd_profile_enable.argtypes = [ctypes.c_int]
+        L.ffd_profile_enable.restype = ctypes.c_int
+        L.ffd_profile_take.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64)]
+        L.ffd_profile_take.restype = ctypes.c_int
         _lib = L
     return _lib
 
 
 EXPORTED = ["ffd_batch", "ffd_batch_workspace_bytes", "ffd_batch_host", "ffd_cdist",
             "ffd_cdist_workspace_bytes", "ffd_validate_batch", "ffd_status_string",
-            "ffd_take_launch_count", "ffd_version"]
+            "ffd_take_launch_count", "ffd_version", "ffd_profile_enable", "ffd_profile_take"]
 
 
 def _norm(norm) -> int:
@@ -114,6 +118,18 @@ def workspace(nbytes: int, device):
         buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
         _ws_cache[key] = buf
     return buf
+
+
+def profile_enable(on: bool = True):
+    lib().ffd_profile_enable(1 if on else 0)
+
+
+def profile_take():
+    """(summed dominant-kernel ms, number of timed launches) since the last take."""
+    ms = ctypes.c_double(0.0)
+    n = ctypes.c_int64(0)
+    _check(lib().ffd_profile_take(ctypes.byref(ms), ctypes.byref(n)), "ffd_profile_take")
+    return ms.value, n.value
 
 
 def launches_taken() -> int:

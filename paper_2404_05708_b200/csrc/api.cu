@@ -56,6 +56,28 @@ static DevInfo dev_info() {
 
 static thread_local int64_t g_launches = 0;
 
+// ---- profiling hook: event pairs around the dominant kernel -----------------
+static std::mutex g_prof_mu;
+static std::atomic<int> g_prof_on{0};
+static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_prof_events;
+
+struct ProfScope {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t st;
+  explicit ProfScope(cudaStream_t s) : st(s) {
+    if (!g_prof_on.load()) return;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, st);
+  }
+  ~ProfScope() {
+    if (!a) return;
+    cudaEventRecord(b, st);
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    g_prof_events.emplace_back(a, b);
+  }
+};
+
 constexpr int kMaxCtasMain = 6;  // cap on resident CTAs/SM used to size scratch
 constexpr int kCtasFb = 1;
 
@@ -150,7 +172,10 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
   int occ = main_e->occupancy();
   if (occ < 1) occ = 1;
   if (occ > kMaxCtasMain) occ = kMaxCtasMain;
-  if (main_e->launch(pb, di.sms * occ, st) != cudaSuccess) return FFD_ERR_CUDA;
+  {
+    ProfScope prof(st);
+    if (main_e->launch(pb, di.sms * occ, st) != cudaSuccess) return FFD_ERR_CUDA;
+  }
   ++g_launches;
 
   if (fb_e) {
@@ -204,6 +229,33 @@ const char* ffd_status_string(int s) {
     case FFD_ERR_WORKSPACE: return "workspace too small";
     default: return "unknown status";
   }
+}
+
+int ffd_profile_enable(int on) {
+  g_prof_on.store(on ? 1 : 0);
+  return FFD_OK;
+}
+
+int ffd_profile_take(double* total_ms, int64_t* launches) {
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    ev.swap(g_prof_events);
+  }
+  double sum = 0.0;
+  int rc = FFD_OK;
+  for (auto& e : ev) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(e.second) != cudaSuccess ||
+        cudaEventElapsedTime(&ms, e.first, e.second) != cudaSuccess)
+      rc = FFD_ERR_CUDA;
+    sum += ms;
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  if (total_ms) *total_ms = sum;
+  if (launches) *launches = (int64_t)ev.size();
+  return rc;
 }
 
 int64_t ffd_take_launch_count(void) {
@@ -303,6 +355,7 @@ int ffd_cdist(const void* setA, int64_t nA, int32_t lenA, const void* setB, int6
   a.out = out;
   a.ld_out = ld_out;
   a.workspace = workspace;
+  ProfScope prof(reinterpret_cast<cudaStream_t>(stream));
   return launch_cdist(a, dev_info().sms, reinterpret_cast<cudaStream_t>(stream), &g_launches);
 }
 

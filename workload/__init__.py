@@ -41,7 +41,7 @@ def lib():
     if _lib is None:
         L = ctypes.CDLL(build())
         P, I64, I32, U64, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64, ctypes.c_double
-        L.ffdgen_lengths.argtypes = [U64, U64, I64, I32, I32, P]
+        L.ffdgen_lengths.argtypes = [U64, U64, I64, I64, I32, I32, P]
         L.ffdgen_walks_f32.argtypes = [U64, U64, I64, I64, P, P, I32, D, D, P]
         L.ffdgen_walks_i32.argtypes = [U64, U64, I64, I64, P, P, I32, I32, I32, P]
         L.ffdgen_walks_unit_f32.argtypes = [U64, U64, I64, I64, P, P, I32, P]
@@ -102,11 +102,11 @@ def _tag(cid: int, what: int) -> int:
     return cid * 16 + what
 
 
-def gen_lengths(cfg: Config, which: str, count: int | None = None) -> np.ndarray:
+def gen_lengths(cfg: Config, which: str, count: int | None = None, first: int = 0) -> np.ndarray:
     count = cfg.pairs if count is None else count
     lo, hi = cfg.len_p if which == "p" else cfg.len_q
     out = np.empty(count, np.int32)
-    lib().ffdgen_lengths(SEED, _tag(cfg.cid, 0 if which == "p" else 1), count, lo, hi, _ptr(out))
+    lib().ffdgen_lengths(SEED, _tag(cfg.cid, 0 if which == "p" else 1), first, count, lo, hi, _ptr(out))
     return out
 
 
@@ -151,13 +151,14 @@ class Batch:
         return int(np.dot(self.lengths[:B].astype(np.int64), self.lengths[B:].astype(np.int64)))
 
 
-def gen_batch(cfg: Config, alloc=None) -> Batch:
-    """Generate a batch config.  `alloc(shape, dtype)` may return writable
-    numpy views (e.g. of pinned torch tensors); default np.empty."""
+def gen_batch(cfg: Config, alloc=None, first: int = 0) -> Batch:
+    """Generate pairs first..first+cfg.pairs-1 of a batch config (pair k depends
+    only on k).  `alloc(shape, dtype)` may return writable numpy views (e.g. of
+    pinned torch tensors); default np.empty."""
     alloc = alloc or (lambda shape, dtype: np.empty(shape, dtype))
     B = cfg.pairs
-    lp = gen_lengths(cfg, "p")
-    lq = gen_lengths(cfg, "q")
+    lp = gen_lengths(cfg, "p", first=first)
+    lq = gen_lengths(cfg, "q", first=first)
     op = np.zeros(B, np.int64)
     oq = np.zeros(B, np.int64)
     if B > 1:
@@ -166,8 +167,8 @@ def gen_batch(cfg: Config, alloc=None) -> Batch:
     dt = np_dtype(cfg)
     p = alloc((int(lp.sum()), cfg.dim), dt)
     q = alloc((int(lq.sum()), cfg.dim), dt)
-    _walks(cfg, 2, lp, op, p)
-    _walks(cfg, 3, lq, oq, q)
+    _walks(cfg, 2, lp, op, p, first=first)
+    _walks(cfg, 3, lq, oq, q, first=first)
     return Batch(p, q, np.concatenate([op, oq]), np.concatenate([lp, lq]), cfg.dim, cfg.norm)
 
 

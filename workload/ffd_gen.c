@@ -72,13 +72,13 @@ static int64_t rng_int(rng_t* r, int64_t lo, int64_t hi) {
   return lo + (int64_t)(m >> 64);
 }
 
-/* lengths[i] ~ U{lo..hi}, i = 0..count-1, stream (seed, tag), one word per curve */
-void ffdgen_lengths(uint64_t seed, uint64_t tag, int64_t count, int32_t lo, int32_t hi,
-                    int32_t* out) {
+/* lengths[i] ~ U{lo..hi} for curve ids first..first+count-1, one word per curve */
+void ffdgen_lengths(uint64_t seed, uint64_t tag, int64_t first, int64_t count, int32_t lo,
+                    int32_t hi, int32_t* out) {
 #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < count; i++) {
     rng_t r;
-    rng_init(&r, seed, tag, (uint64_t)i);
+    rng_init(&r, seed, tag, (uint64_t)(first + i));
     out[i] = (int32_t)rng_int(&r, lo, hi);
   }
 }

@@ -19,7 +19,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libffd.so")
+LIB_PATH = os.environ.get("FFD_LIB", os.path.join(_HERE, "libffd.so"))
 
 L1, L2, LINF, SQL2 = 1, 2, 3, 4
 NORMS = {"l1": L1, "l2": L2, "linf": LINF, "sql2": SQL2}

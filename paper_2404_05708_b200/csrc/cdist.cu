@@ -1,9 +1,265 @@
-// cdist.cu — placeholder
+// cdist.cu — all-pairs discrete Fréchet distances between two dense curve sets.
+//
+// out[a - row_begin][b] = δ_dF(A_a, B_b) (PAPER Eq. (1), evaluated as
+// in strip.cuh).  B200 design (DESIGN.md §"cdist kernel"):
+//   * A warp is split into 32/W segments of W lanes; each segment keeps one
+//     A-curve (the rows, ≤ W·R points) in registers for the whole work item —
+//     rows are loaded once, never reloaded.  Lane s of a segment owns rows
+//     [sR, sR+R) and processes column t − s at step t; boundary values move
+//     down the segment with __shfl_up_sync(width = W).
+//   * All segments of a warp stream the same tile of B curves through a
+//     per-warp shared-memory ring (each element read with a broadcast LDS):
+//     [sentinel, B_b0 points, sentinel, B_b0+1 points, …, sentinel].  The
+//     sentinel column (+inf) resets the DP between B curves; the top lane of
+//     each segment sees the corner value 0 at the sentinel.
+//   * All B curves have the same length, so the stream is periodic with
+//     period P = lenB + 1: the step at which a segment's last lane holds a
+//     finished δ is known to the whole warp, and the results are stored with
+//     one predicated store per period (no per-lane event checks).
+//   * Work items (4 A-curves × a tile of B curves) are popped dynamically by
+//     persistent warps; a rank's shard is a contiguous row range of A.
+#include <climits>
+
 #include "cdist.cuh"
 #include "ffd.h"
+#include "strip.cuh"
+
 namespace ffd {
-size_t cdist_workspace_bytes() { return 0; }
-int launch_cdist(const CdistArgs& a, int sms, cudaStream_t st, int64_t* launches) {
-  return FFD_ERR_UNSUPPORTED;
+
+constexpr int kCdTile = 128;  // B curves per work item
+
+struct CdistProblem {
+  const float* A;
+  const float* B;
+  int64_t nA, nB;
+  int lenA, lenB;
+  int64_t row_begin, row_end;
+  float* out;
+  int64_t ld_out;
+  int* counter;
+  int64_t n_items;
+  int64_t tiles_b;
+};
+
+template <int KIND, int D, int W, int R, int FIN>
+__global__ void __launch_bounds__(kWarp* kWarpsPerCta, kMinCtasPerSm)
+    cdist_kernel(const CdistProblem pb) {
+  using C = SCfg<float, KIND, D, false>;
+  static_assert(!C::XSQ, "cdist: fp32 inputs");
+  constexpr int SEG = kWarp / W;
+  constexpr int EW = C::EW;
+  __shared__ uint4 ring_all[kWarpsPerCta][kRing * EW];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = lane % W;        // lane index inside the segment
+  const int seg = lane / W;      // segment index inside the warp
+  uint4* ring = ring_all[warp];
+  const int P = pb.lenB + 1;     // stream period
+
+  while (true) {
+    int64_t item = 0;
+    if (lane == 0) item = atomicAdd(pb.counter, 1);
+    item = __shfl_sync(0xffffffffu, (long long)item, 0);
+    if (item >= pb.n_items) break;
+    const int64_t ablk = item / pb.tiles_b;
+    const int64_t tb = item % pb.tiles_b;
+    const int64_t a = pb.row_begin + ablk * SEG + seg;        // this segment's A curve
+    const bool a_ok = a < pb.row_end;
+    const int64_t b0 = tb * kCdTile;
+    const int nb = (int)min((int64_t)kCdTile, pb.nB - b0);
+    const int S = nb * P + 1;                                  // stream positions
+
+    // rows of this segment's A curve (padded by repeating the last point)
+    float x[C::NS][R];
+    {
+      const float* ap = pb.A + (a_ok ? a : pb.row_begin) * (int64_t)pb.lenA * D;
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        const int row = min(s * R + r, pb.lenA - 1);
+#pragma unroll
+        for (int c = 0; c < D; c++) x[c][r] = __ldg(ap + (int64_t)row * D + c);
+      }
+    }
+    // column element loader: position pos -> sentinel or B point
+    const float* bbase = pb.B + b0 * (int64_t)pb.lenB * D;
+    auto load_pt = [&](int pos, float (&v)[D]) {
+      if (pos < S) {
+        const int b = pos / P, k = pos - b * P;
+        if (k == 0) {
+#pragma unroll
+          for (int c = 0; c < D; c++) v[c] = finf();
+        } else {
+          const float* bp = bbase + ((int64_t)b * pb.lenB + (k - 1)) * D;
+#pragma unroll
+          for (int c = 0; c < D; c++) v[c] = __ldg(bp + c);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < D; c++) v[c] = finf();
+      }
+    };
+    auto store_el = [&](int pos, const float (&v)[D]) {
+      alignas(16) float e[C::EBYTES / 4];
+#pragma unroll
+      for (int i = 0; i < C::EBYTES / 4; i++) e[i] = 0.f;
+#pragma unroll
+      for (int c = 0; c < D; c++) e[c] = v[c];
+      uint4* dst = ring + (pos & kRingMask) * EW;
+#pragma unroll
+      for (int w = 0; w < EW; w++) dst[w] = reinterpret_cast<const uint4*>(e)[w];
+    };
+    float pre[D];
+    {
+      float v0[D];
+      load_pt(lane, v0);
+      store_el(lane, v0);
+      load_pt(32 + lane, pre);
+    }
+    __syncwarp();
+
+    float c[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) c[r] = finf();
+    float diag = finf();
+    // one step: element, boundary value from the lane above, R cells.  `top` is
+    // what the segment's first lane sees above its first row: the corner value
+    // 0 on a sentinel column (t ≡ 0 mod P), +inf otherwise.
+    auto step = [&](int t, float top) {
+      const int g = t - s;
+      alignas(16) float e[C::EBYTES / 4];
+      {
+        const uint4* src = ring + (g & kRingMask) * EW;
+#pragma unroll
+        for (int w = 0; w < EW; w++) reinterpret_cast<uint4*>(e)[w] = src[w];
+      }
+      const float upv = __shfl_up_sync(0xffffffffu, c[R - 1], 1, W);
+      const float up = (s == 0) ? top : upv;
+      float dist[R];
+      cell_dists<float, KIND, D, R, false>(x, e, dist);
+      float u = up, dg = diag;
+      diag = up;
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        const float m = fminf(fminf(u, dg), c[r]);
+        const float nv = fmaxf(m, dist[r]);
+        dg = c[r];
+        c[r] = nv;
+        u = nv;
+      }
+    };
+    const int total = S + W - 1;
+    int next_out = P + W - 1;  // segment-last lanes enter the sentinel after B curve out_b
+    int out_b = 0;
+    int next_refill = 32;
+    int next_sent = 0;         // segment-first lanes on a sentinel column
+    int t = 0;
+    while (t < total) {
+      const int stop = min(min(min(next_refill, next_out), next_sent), total);
+#pragma unroll 2
+      for (; t < stop; ++t) step(t, finf());
+      if (t >= total) break;
+      if (t == next_refill) {
+        store_el(t + lane, pre);
+        load_pt(t + 32 + lane, pre);
+        next_refill += 32;
+        __syncwarp();
+      }
+      if (t == next_out) {
+        // segment-last lanes hold δ(A_a, B_{b0+out_b}): column P·(out_b+1) − 1 is done
+        if (s == W - 1 && a_ok) {
+          float v = c[R - 1];
+          if constexpr (FIN == F_SQRT) v = __fsqrt_rn(v);
+          pb.out[(a - pb.row_begin) * pb.ld_out + b0 + out_b] = v;
+        }
+        ++out_b;
+        next_out += P;
+      }
+      if (t == next_sent) {
+        step(t, 0.f);
+        ++t;
+        next_sent += P;
+      }
+    }
+    __syncwarp();
+  }
 }
+
+// ---- dispatch ----------------------------------------------------------------
+template <int KIND, int D, int W, int R, int FIN>
+static cudaError_t launch_one(const CdistProblem& pb, int sms, cudaStream_t st) {
+  auto k = cdist_kernel<KIND, D, W, R, FIN>;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kWarp * kWarpsPerCta, 0);
+  if (occ < 1) occ = 1;
+  k<<<sms * occ, kWarp * kWarpsPerCta, 0, st>>>(pb);
+  return cudaGetLastError();
+}
+
+// shapes: (W, R) with W·R ≥ lenA, R ≤ 16; pick the smallest capacity
+template <int KIND, int D, int FIN>
+static cudaError_t launch_shape(const CdistProblem& pb, int sms, cudaStream_t st, int W, int R) {
+#define FFD_CD(WW, RR) \
+  if (W == WW && R == RR) return launch_one<KIND, D, WW, RR, FIN>(pb, sms, st);
+  FFD_CD(8, 4) FFD_CD(8, 8) FFD_CD(8, 16) FFD_CD(16, 12) FFD_CD(16, 16) FFD_CD(32, 12)
+  FFD_CD(32, 16)
+#undef FFD_CD
+  return cudaErrorInvalidValue;
+}
+
+static void pick_shape(int rows, int& W, int& R) {
+  static const int shapes[][2] = {{8, 4}, {8, 8}, {8, 16}, {16, 12}, {16, 16}, {32, 12}, {32, 16}};
+  for (auto& sh : shapes)
+    if (sh[0] * sh[1] >= rows) {
+      W = sh[0];
+      R = sh[1];
+      return;
+    }
+  W = 0;
+  R = 0;
+}
+
+size_t cdist_workspace_bytes() { return 256; }
+
+int launch_cdist(const CdistArgs& a, int sms, cudaStream_t st, int64_t* launches) {
+  if (a.dtype != FFD_F32) return FFD_ERR_UNSUPPORTED;
+  if (a.dim != 2 && a.dim != 3) return FFD_ERR_UNSUPPORTED;
+  int W = 0, R = 0;
+  pick_shape(a.lenA, W, R);
+  if (!W) return FFD_ERR_UNSUPPORTED;  // rows longer than one warp band
+  if ((int64_t)a.lenB + 1 > INT_MAX / (kCdTile + 1)) return FFD_ERR_UNSUPPORTED;
+  CdistProblem pb{};
+  pb.A = reinterpret_cast<const float*>(a.A);
+  pb.B = reinterpret_cast<const float*>(a.B);
+  pb.nA = a.nA;
+  pb.nB = a.nB;
+  pb.lenA = a.lenA;
+  pb.lenB = a.lenB;
+  pb.row_begin = a.row_begin;
+  pb.row_end = a.row_end;
+  pb.out = reinterpret_cast<float*>(a.out);
+  pb.ld_out = a.ld_out;
+  pb.counter = reinterpret_cast<int*>(a.workspace);
+  const int seg = kWarp / W;
+  const int64_t rows = a.row_end - a.row_begin;
+  pb.tiles_b = (a.nB + kCdTile - 1) / kCdTile;
+  pb.n_items = ((rows + seg - 1) / seg) * pb.tiles_b;
+  if (pb.n_items > INT_MAX) return FFD_ERR_UNSUPPORTED;
+  if (cudaMemsetAsync(pb.counter, 0, sizeof(int), st) != cudaSuccess) return FFD_ERR_CUDA;
+  cudaError_t e = cudaErrorInvalidValue;
+  const int kind = a.norm == FFD_L1 ? K_L1 : (a.norm == FFD_LINF ? K_LINF : K_SQ);
+  const bool sq = (a.norm == FFD_L2);
+  if (a.dim == 2) {
+    if (kind == K_SQ) e = sq ? launch_shape<K_SQ, 2, F_SQRT>(pb, sms, st, W, R)
+                             : launch_shape<K_SQ, 2, F_NONE>(pb, sms, st, W, R);
+    else if (kind == K_L1) e = launch_shape<K_L1, 2, F_NONE>(pb, sms, st, W, R);
+    else e = launch_shape<K_LINF, 2, F_NONE>(pb, sms, st, W, R);
+  } else {
+    if (kind == K_SQ) e = sq ? launch_shape<K_SQ, 3, F_SQRT>(pb, sms, st, W, R)
+                             : launch_shape<K_SQ, 3, F_NONE>(pb, sms, st, W, R);
+    else if (kind == K_L1) e = launch_shape<K_L1, 3, F_NONE>(pb, sms, st, W, R);
+    else e = launch_shape<K_LINF, 3, F_NONE>(pb, sms, st, W, R);
+  }
+  ++*launches;
+  return e == cudaSuccess ? FFD_OK : FFD_ERR_CUDA;
+}
+
 }  // namespace ffd

@@ -1,0 +1,68 @@
+"""Parity of ffd_cdist (CUDA, through the C ABI) against the CPU oracle."""
+import numpy as np
+import pytest
+
+import oracle
+import workload
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ffd():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2404_05708_b200 as ffd
+    ffd.lib()
+    return ffd
+
+
+def check(got, A, B, ia, ib, norm):
+    ref = oracle.cdist_entries(A, B, ia, ib, norm)
+    mir = oracle.cdist_entries(A, B, ia, ib, norm, mirror=True)
+    err = np.abs(got.astype(np.float64) - ref)
+    assert (err <= 1e-5 * np.abs(ref)).all(), f"max rel err {(err / np.maximum(np.abs(ref), 1e-30)).max()}"
+    assert np.array_equal(got, mir), f"{(got != mir).sum()} entries differ from the fp32 mirror"
+
+
+@pytest.mark.parametrize("lenA,lenB,norm,dim", [(128, 128, "l2", 2), (37, 90, "l2", 2), (128, 200, "l1", 2),
+                                                (250, 64, "linf", 2), (500, 33, "sql2", 2), (1, 5, "l2", 2),
+                                                (64, 1, "l2", 2), (100, 120, "l2", 3)])
+def test_small_full_matrix(ffd, lenA, lenB, norm, dim):
+    cfg = workload.CONFIGS[4].scaled(nA=23, nB=301, length=lenA, dim=dim)
+    A = workload.gen_set(cfg, "A")
+    B = workload.gen_set(cfg.scaled(length=lenB), "B")
+    got = ffd.cdist(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), norm=norm).cpu().numpy()
+    ia = np.repeat(np.arange(23), 301)
+    ib = np.tile(np.arange(301), 23)
+    check(got.ravel(), A, B, ia, ib, norm)
+
+
+def test_shard_rows_and_ld(ffd):
+    cfg = workload.CONFIGS[4].scaled(nA=50, nB=140, length=128)
+    A = torch.from_numpy(workload.gen_set(cfg, "A")).cuda()
+    B = torch.from_numpy(workload.gen_set(cfg, "B")).cuda()
+    full = ffd.cdist(A, B, "l2")
+    out = torch.full((20, 150), -1.0, device="cuda")
+    ffd.cdist(A, B, "l2", rows=(13, 33), out=out, ld_out=150)
+    assert torch.equal(out[:, :140], full[13:33])
+    assert (out[:, 140:] == -1).all()          # nothing written past nB
+
+
+def test_config4_full_size_sampled(ffd):
+    """Full BASELINE config 4 (20k × 20k, L=128) in the bench launch shape;
+    sampled entries + one full row and column checked against the oracle."""
+    cfg = workload.CONFIGS[4]
+    A = workload.gen_set(cfg, "A")
+    B = workload.gen_set(cfg, "B")
+    got = ffd.cdist(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), "l2")
+    n = 3000
+    ia = workload.sample_indices(cfg, 0, n, cfg.nA)
+    ib = workload.sample_indices(cfg, 1, n, cfg.nB)
+    ia = np.concatenate([ia, np.full(400, 12345), np.arange(400) * 50])
+    ib = np.concatenate([ib, np.arange(400) * 50, np.full(400, 777)])
+    sel = got[torch.from_numpy(ia).cuda(), torch.from_numpy(ib).cuda()].cpu().numpy()
+    check(sel, A, B, ia, ib, "l2")
+    # properties at full size: finite, non-negative, diagonal-free sanity
+    assert torch.isfinite(got).all() and (got >= 0).all()

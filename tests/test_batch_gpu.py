@@ -146,6 +146,51 @@ def test_identity_and_symmetry(ffd):
     assert np.array_equal(o1, o2)
 
 
+@pytest.mark.parametrize("dim", [1, 2, 3, 4])
+@pytest.mark.parametrize("norm", ["l1", "l2", "linf", "sql2"])
+def test_all_norms_dims_f32(ffd, norm, dim):
+    rng = np.random.default_rng(100 + dim * 7 + len(norm))
+    b = make_batch(rng, 150, 1, 700, dim=dim)
+    out = ffd.batch(*to_dev(b), norm=norm)
+    check_float(out.cpu().numpy(), b, norm)
+
+
+@pytest.mark.parametrize("dim", [1, 2, 3, 4])
+@pytest.mark.parametrize("norm", ["l1", "linf", "sql2"])
+def test_all_norms_dims_int(ffd, norm, dim):
+    rng = np.random.default_rng(200 + dim * 7 + len(norm))
+    b = make_batch(rng, 150, 1, 700, dim=dim, kind="i")
+    out = ffd.batch(*to_dev(b), norm=norm)
+    check_int(out.cpu().numpy(), b, norm)
+    # and outside the fp32-exact window (exact int64 tier)
+    b2 = make_batch(rng, 60, 1, 300, dim=dim, kind="i", scale=20000.0)
+    out2 = ffd.batch(*to_dev(b2), norm=norm)
+    check_int(out2.cpu().numpy(), b2, norm)
+
+
+def test_validate(ffd):
+    rng = np.random.default_rng(12)
+    b = make_batch(rng, 20, 1, 50)
+    args = to_dev(b)
+    assert ffd.validate(*args) == 0
+    bad = args[0].clone()
+    bad[3, 1] = float("nan")
+    assert ffd.validate(bad, *args[1:]) == -5
+    lens = args[3].clone()
+    lens[2] = 0
+    assert ffd.validate(args[0], args[1], args[2], lens) == -4
+    offs = args[2].clone()
+    offs[25] = 10**9
+    assert ffd.validate(args[0], args[1], offs, args[3]) == -7
+    bi = make_batch(rng, 5, 1, 20, kind="i")
+    ai = to_dev(bi)
+    assert ffd.validate(*ai) == 0
+    big_p, big_q = ai[0].clone(), ai[1].clone()
+    big_p[0, :] = 2**31 - 1          # first point of pair 0's p
+    big_q[0, :] = -(2**31)           # first point of pair 0's q
+    assert ffd.validate(big_p, big_q, ai[2], ai[3]) == -6
+
+
 def test_batch_host_matches_device(ffd):
     cfg = workload.CONFIGS[2].scaled(pairs=500)
     b = workload.gen_batch(cfg)

@@ -1,0 +1,95 @@
+"""Parity of the long-pair wavefront kernel (pairs too long for one warp band
+scratch; BASELINE config 5) against the CPU oracle."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workload
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+GOLD_C5 = os.path.join(os.path.dirname(__file__), "golden", "c5_expected.json")
+
+
+@pytest.fixture(scope="module")
+def ffd():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2404_05708_b200 as ffd
+    ffd.lib()
+    return ffd
+
+
+def walk(rng, n, dim=2, kind="f", step=1):
+    if kind == "i":
+        return np.cumsum(rng.integers(-step, step + 1, size=(n, dim)), axis=0).astype(np.int32)
+    return np.cumsum(rng.normal(size=(n, dim)), axis=0).astype(np.float32)
+
+
+def run_pairs(ffd, pairs, norm):
+    P = np.concatenate([p for p, _ in pairs])
+    Q = np.concatenate([q for _, q in pairs])
+    lp = np.array([len(p) for p, _ in pairs], np.int32)
+    lq = np.array([len(q) for _, q in pairs], np.int32)
+    op = np.concatenate([[0], np.cumsum(lp)[:-1]]).astype(np.int64)
+    oq = np.concatenate([[0], np.cumsum(lq)[:-1]]).astype(np.int64)
+    args = [torch.from_numpy(a).cuda() for a in (P, Q, np.concatenate([op, oq]), np.concatenate([lp, lq]))]
+    return ffd.batch(*args, norm=norm).cpu().numpy()
+
+
+@pytest.mark.parametrize("norm", ["l2", "l1", "linf"])
+def test_long_pairs_f32(ffd, norm):
+    rng = np.random.default_rng(3)
+    shapes = [(600, 5000), (5000, 6000), (3000, 3000), (7000, 600), (40, 70)]
+    pairs = [(walk(rng, n), walk(rng, m)) for n, m in shapes]
+    got = run_pairs(ffd, pairs, norm)
+    for k, (p, q) in enumerate(pairs):
+        ref = oracle.pair(p, q, norm, form="linear")
+        mir = oracle.pair(p, q, norm, form="mirror")
+        assert abs(got[k] - ref) <= 1e-5 * abs(ref), (k, got[k], ref)
+        assert got[k] == mir, (k, got[k], mir)
+
+
+def test_long_pairs_int_exact(ffd):
+    rng = np.random.default_rng(4)
+    shapes = [(4000, 5000), (600, 4000)]
+    pairs = [(walk(rng, n, kind="i"), walk(rng, m, kind="i")) for n, m in shapes]
+    got = run_pairs(ffd, pairs, "sql2")
+    for k, (p, q) in enumerate(pairs):
+        assert got[k] == oracle.pair(p, q, "sql2", form="linear")
+
+
+@pytest.mark.parametrize("ctas,expect_ok", [("3", True), ("6", True), ("1", False)])
+def test_long_pair_rows_per_lane(ffd, ctas, expect_ok):
+    """fewer CTAs force R = 32 / 16 (all bands must be co-resident); a pair that does
+    not fit even at R = 32 gets NaN (documented limit)"""
+    rng = np.random.default_rng(5)
+    pairs = [(walk(rng, 20000), walk(rng, 20000)), (walk(rng, 300), walk(rng, 5000))]
+    os.environ["FFD_LONG_CTAS"] = ctas
+    try:
+        got = run_pairs(ffd, pairs, "l2")
+    finally:
+        del os.environ["FFD_LONG_CTAS"]
+    p, q = pairs[0]
+    if expect_ok:
+        assert got[0] == oracle.pair(p, q, "l2", form="mirror")
+    else:
+        assert np.isnan(got[0])
+    p, q = pairs[1]
+    assert got[1] == oracle.pair(p, q, "l2", form="mirror")
+
+
+def test_config5_full_size(ffd):
+    if not os.path.exists(GOLD_C5):
+        pytest.skip("golden values not generated (scripts/make_golden_c5.py)")
+    gold = json.load(open(GOLD_C5))
+    p, q = workload.gen_long_pair(workload.CONFIGS[5])
+    assert hashlib.sha256(p.tobytes() + q.tobytes()).hexdigest() == gold["input_sha256"]
+    for norm, ref in gold["expected"].items():
+        got = run_pairs(ffd, [(p, q)], norm)[0]
+        assert abs(got - ref) <= 1e-5 * abs(ref), (norm, got, ref)

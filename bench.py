@@ -122,26 +122,77 @@ def run_oracle_timed(b, cfg, threads):
     return time.perf_counter() - t0
 
 
+def oracle_runner(cfg, target_cells: float, cores: int):
+    """(callable timing one oracle pass, cells per pass, sample description) for a
+    bounded sample of config `cfg` (batch: leading pairs; cdist: seeded entries;
+    long pair: the leading sub-problem of the pair)."""
+    import oracle
+    if cfg.kind == "batch":
+        b, k = oracle_sample(cfg, target_cells)
+        return (lambda: run_oracle_timed(b, cfg, cores)), b.cells(), \
+            f"first {k} pairs of {cfg.name} ({b.cells():.3g} cells), plain C table DP, OpenMP over pairs"
+    if cfg.kind == "cdist":
+        cnt = max(1, int(target_cells // (cfg.length * cfg.length)))
+        ia = workload.sample_indices(cfg, 0, cnt, cfg.nA)
+        ib = workload.sample_indices(cfg, 1, cnt, cfg.nB)
+        A = workload.gen_set(cfg, "A")
+        B = workload.gen_set(cfg, "B")
+
+        def run():
+            t0 = time.perf_counter()
+            oracle.cdist_entries(A, B, ia, ib, cfg.norm, threads=cores)
+            return time.perf_counter() - t0
+        cells = cnt * cfg.length * cfg.length
+        return run, cells, f"{cnt} seeded (a, b) entries of {cfg.name} ({cells:.3g} cells), plain C table DP"
+    # long pair: leading s×s sub-problem, one per norm, run concurrently (one core each)
+    p, q = workload.gen_long_pair(cfg)
+    s = int(min(p.shape[0], (target_cells / len(cfg.norms)) ** 0.5))
+    from concurrent.futures import ThreadPoolExecutor
+
+    def run():
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(len(cfg.norms)) as ex:
+            list(ex.map(lambda nm: oracle.pair(p[:s], q[:s], nm, form="linear"), cfg.norms))
+        return time.perf_counter() - t0
+    cells = s * s * len(cfg.norms)
+    return run, cells, (f"leading {s}x{s} sub-problem of {cfg.name} under {'/'.join(cfg.norms)} "
+                        f"({cells:.3g} cells), fp64 Alg. 5 linear form, one core per norm")
+
+
+def cpu_baseline_line(args, cfg, ws):
+    """The oracle timed on the host cores on a bounded sample (rank 0, N = 1 only)."""
+    if ws != 1 or args.no_cpu_baseline:
+        return None
+    cores = cpu_cores()
+    run, ccells, sample = oracle_runner(cfg, args.cpu_cells, cores)
+    t = run()
+    if cfg.kind == "long":
+        cores = len(cfg.norms)
+    return {"value": ccells / t / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{sample} (oracle/ffd_oracle.c), {t:.1f} s"}
+
+
 def bench_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
     cfg = workload.CONFIGS[args.config]
     cores = cpu_cores()
-    b, k = oracle_sample(cfg, 3e8)
-    cells = b.cells()
+    run, cells, sample = oracle_runner(cfg, 3e8, cores)
     for _ in range(args.warmup):
-        run_oracle_timed(b, cfg, cores)
-    t = sum(run_oracle_timed(b, cfg, cores) for _ in range(args.steps))
+        run()
+    t = sum(run() for _ in range(args.steps))
     value = cells * args.steps / t / 1e9
+    if cfg.kind == "long":
+        cores = len(cfg.norms)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-        "data": "synthetic", "config": {"workload": cfg.name, "sample_pairs": k, "sample_cells": cells},
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int64" if cfg.dtype == "i32" else "f64",
+        "data": "synthetic", "config": {"workload": cfg.name, "sample_cells": cells},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": f"first {k} pairs of {cfg.name} ({cells:.3g} cells) per step, "
-                                   f"plain C table DP, OpenMP over pairs"},
+                         "sample": sample + " (per step)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -266,14 +317,7 @@ def bench_ffd(args):
         "frac_at_measured_clock": achieved / (sms * 128 * f_meas / ops / 1e9),
     }
 
-    cpu = None
-    if ws == 1 and not args.no_cpu_baseline:
-        cores = cpu_cores()
-        sb, k = oracle_sample(cfg, args.cpu_cells)
-        t = run_oracle_timed(sb, cfg, cores)
-        cpu = {"value": sb.cells() / t / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"first {k} pairs of {cfg.name} ({sb.cells():.3g} cells), plain C table DP "
-                         f"(oracle/ffd_oracle.c), OpenMP over pairs, {t:.1f} s"}
+    cpu = cpu_baseline_line(args, cfg, ws)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -399,6 +443,7 @@ def bench_cdist(args):
                        "parallelism": f"rows of A over {ws} GPU(s) + all_gather_into_tensor (NCCL)",
                        "l2": "B (20 MB) L2-resident by design; output 1.6 GB streamed"},
             "clocks": clocks,
+            "cpu_baseline": cpu_baseline_line(args, cfg, ws),
             "roofline": {"bound": "alu", "achieved": ach, "peak": peak, "unit": UNIT, "frac": ach / peak,
                          "traffic": args.traffic, "kernel": "cdist_kernel (fp32 L2, W=8 R=16)",
                          "kernel_ms": kern_max, "ops_per_cell": ops,
@@ -414,6 +459,120 @@ def bench_cdist(args):
     if ws > 1:
         dist.destroy_process_group()
     return 0
+
+
+def bench_long(args):
+    """Config 5: one pair n = m = 262,144 (2-D fp32), the long-pair wavefront kernel
+    (SURVEY §8(a) a8), under L1, L2 and L∞; one step = the three calls.  Replicas only
+    (the pair does not shard): with N ranks every rank runs its own copy."""
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local if ws > 1 else 0)
+    torch.cuda.set_device(dev)
+    import paper_2404_05708_b200 as ffd
+    ffd.lib()
+    cfg = workload.CONFIGS[5]
+    p_h, q_h = workload.gen_long_pair(cfg)
+    n, m = p_h.shape[0], q_h.shape[0]
+    p = torch.from_numpy(p_h).to(dev)
+    q = torch.from_numpy(q_h).to(dev)
+    off = torch.tensor([0, 0], dtype=torch.int64, device=dev)
+    lens = torch.tensor([n, m], dtype=torch.int32, device=dev)
+    outs = {nm: torch.empty(1, dtype=torch.float32, device=dev) for nm in cfg.norms}
+    stream = torch.cuda.current_stream(dev)
+    cells = n * m
+
+    def step():
+        for nm in cfg.norms:
+            ffd.batch(p, q, off, lens, norm=nm, out=outs[nm])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ffd.launches_taken()
+    ffd.profile_take()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(dev.index)
+    per_norm = {nm: 0.0 for nm in cfg.norms}
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with sampler:
+        e0.record(stream)
+        for _ in range(args.steps):
+            for nm in cfg.norms:
+                ffd.profile_enable(True)
+                ffd.batch(p, q, off, lens, norm=nm, out=outs[nm])
+                ffd.profile_enable(False)
+                per_norm[nm] += ffd.profile_take()[0]
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = ffd.launches_taken() // args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t[0])
+    vals = {nm: float(outs[nm].item()) for nm in cfg.norms}
+    # end to end: host points in, three results out, per step
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p_pin = torch.from_numpy(p_h).pin_memory()
+    q_pin = torch.from_numpy(q_h).pin_memory()
+    res_h = torch.empty(len(cfg.norms), dtype=torch.float32, pin_memory=True)
+    e2.record(stream)
+    for _ in range(args.steps):
+        p.copy_(p_pin, non_blocking=True)
+        q.copy_(q_pin, non_blocking=True)
+        step()
+        res_h.copy_(torch.cat([outs[nm] for nm in cfg.norms]), non_blocking=True)
+    e3.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e2.elapsed_time(e3) / args.steps
+    if rank == 0:
+        clocks = sampler.summary()
+        f_max = (clocks["sm_max_mhz"] or SM_MAX_MHZ_NOMINAL) * 1e6
+        f_meas = (clocks["sm_mhz"] or SM_MAX_MHZ_NOMINAL) * 1e6
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        ops = OPS_LONG
+        kern = {nm: per_norm[nm] / args.steps for nm in cfg.norms}
+        ach = {nm: cells / (kern[nm] * 1e-3) / 1e9 for nm in cfg.norms}
+        peak = {nm: sms * 128 * f_max / ops[nm] / 1e9 for nm in cfg.norms}
+        line = {
+            "metric": METRIC, "value": ws * 3 * cells / (ms_max * 1e-3) / 1e9, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg.name, "n": n, "m": m, "norms": list(cfg.norms),
+                       "cells_per_step": 3 * cells, "parallelism": "replicas only (one pair per GPU)",
+                       "l2": "inputs 4.2 MB (L2-resident); the DP state never leaves the SMs"},
+            "clocks": clocks,
+            "cpu_baseline": cpu_baseline_line(args, cfg, ws),
+            "roofline": {"bound": "alu", "achieved": ach["l2"], "peak": peak["l2"], "unit": UNIT,
+                         "frac": ach["l2"] / peak["l2"], "traffic": args.traffic,
+                         "kernel": "long_kernel (fp32 L2)", "kernel_ms": kern["l2"], "ops_per_cell": ops["l2"],
+                         "per_norm": {nm: {"kernel_ms": kern[nm], "achieved": ach[nm], "peak": peak[nm],
+                                           "frac": ach[nm] / peak[nm], "ops_per_cell": ops[nm]}
+                                      for nm in cfg.norms},
+                         "frac_at_measured_clock": ach["l2"] / (sms * 128 * f_meas / ops["l2"] / 1e9)},
+            "e2e": {"value": ws * 3 * cells / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": p_h.nbytes + q_h.nbytes, "d2h_bytes_per_step": 4 * len(cfg.norms)},
+            "results": vals,
+            "gpu_launches": launches * args.steps, "gpu_launches_per_step": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+# slots per cell of the minimal fp32 D=2 cell per norm (DESIGN.md §8): L1 = 2 (FSUB2)
+# + 1 (FADD |a|+|b|) + 2 (FMNMX3) + 1 (FMNMX); L2 = 7; L∞ = 2 (FSUB2) + 1 (FMNMX |a|,|b|)
+# + 2 + 1
+OPS_LONG = {"l1": 6, "l2": 7, "linf": 6}
 
 
 def main():
@@ -433,8 +592,11 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return bench_reference(args)
-    if workload.CONFIGS[args.config].kind == "cdist":
+    kind = workload.CONFIGS[args.config].kind
+    if kind == "cdist":
         return bench_cdist(args)
+    if kind == "long":
+        return bench_long(args)
     return bench_ffd(args)
 
 

@@ -116,10 +116,11 @@ int ffd_validate_batch(const void* p, int64_t np, const void* q, int64_t nq,
 
 /* ---------------------------------------------------------------------------
  * Profiling hook (benchmarks): while enabled, every ffd_batch / ffd_cdist call
- * records a CUDA event pair on its stream around its dominant kernel (the
- * batch / cdist / long-pair DP kernel).  ffd_profile_take() waits for the
- * recorded events, writes the summed kernel milliseconds and the number of
- * timed launches, and clears the record.  Host-side, thread-safe.
+ * records a CUDA event pair on its stream around each of its DP kernels (batch
+ * main tier, exact int64 tier, long-pair wavefront, cdist).  ffd_profile_take()
+ * waits for the recorded events and writes, for the DOMINANT kernel (the one
+ * with the largest summed time), its summed milliseconds and its number of
+ * timed launches; then it clears the record.  Host-side, thread-safe.
  * ------------------------------------------------------------------------- */
 int ffd_profile_enable(int on);
 int ffd_profile_take(double* total_ms, int64_t* launches);

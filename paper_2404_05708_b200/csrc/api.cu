@@ -59,12 +59,17 @@ static thread_local int64_t g_launches = 0;
 // ---- profiling hook: event pairs around the dominant kernel -----------------
 static std::mutex g_prof_mu;
 static std::atomic<int> g_prof_on{0};
-static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_prof_events;
+struct ProfRec {
+  int tag;  // which kernel: 0 batch main tier, 1 exact int64 tier, 2 long pair, 3 cdist
+  cudaEvent_t a, b;
+};
+static std::vector<ProfRec> g_prof_events;
 
 struct ProfScope {
   cudaEvent_t a = nullptr, b = nullptr;
   cudaStream_t st;
-  explicit ProfScope(cudaStream_t s) : st(s) {
+  int tag;
+  ProfScope(cudaStream_t s, int t) : st(s), tag(t) {
     if (!g_prof_on.load()) return;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
@@ -74,7 +79,7 @@ struct ProfScope {
     if (!a) return;
     cudaEventRecord(b, st);
     std::lock_guard<std::mutex> g(g_prof_mu);
-    g_prof_events.emplace_back(a, b);
+    g_prof_events.push_back(ProfRec{tag, a, b});
   }
 };
 
@@ -173,7 +178,7 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
   if (occ < 1) occ = 1;
   if (occ > kMaxCtasMain) occ = kMaxCtasMain;
   {
-    ProfScope prof(st);
+    ProfScope prof(st, 0);
     if (main_e->launch(pb, di.sms * occ, st) != cudaSuccess) return FFD_ERR_CUDA;
   }
   ++g_launches;
@@ -187,6 +192,7 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
     fb.fb_list = nullptr;
     fb.fb_count = nullptr;
     std::memcpy(fb.rmap, fb_e->rmap, sizeof(fb.rmap));
+    ProfScope prof(st, 1);
     if (fb_e->launch(fb, di.sms * kCtasFb, st) != cudaSuccess) return FFD_ERR_CUDA;
     ++g_launches;
   }
@@ -204,6 +210,7 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
   la.list = ws.long_list;
   la.list_count = ws.counters + kCtrLong;
   la.out = out;
+  ProfScope prof(st, 2);
   if (launch_long_pairs(la, di.sms, st, &g_launches) != cudaSuccess) return FFD_ERR_CUDA;
   return FFD_OK;
 }
@@ -237,24 +244,28 @@ int ffd_profile_enable(int on) {
 }
 
 int ffd_profile_take(double* total_ms, int64_t* launches) {
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  std::vector<ProfRec> ev;
   {
     std::lock_guard<std::mutex> g(g_prof_mu);
     ev.swap(g_prof_events);
   }
-  double sum = 0.0;
+  double sum[4] = {0, 0, 0, 0};
+  int64_t cnt[4] = {0, 0, 0, 0};
   int rc = FFD_OK;
   for (auto& e : ev) {
     float ms = 0.f;
-    if (cudaEventSynchronize(e.second) != cudaSuccess ||
-        cudaEventElapsedTime(&ms, e.first, e.second) != cudaSuccess)
+    if (cudaEventSynchronize(e.b) != cudaSuccess || cudaEventElapsedTime(&ms, e.a, e.b) != cudaSuccess)
       rc = FFD_ERR_CUDA;
-    sum += ms;
-    cudaEventDestroy(e.first);
-    cudaEventDestroy(e.second);
+    sum[e.tag] += ms;
+    cnt[e.tag] += 1;
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
   }
-  if (total_ms) *total_ms = sum;
-  if (launches) *launches = (int64_t)ev.size();
+  int top = 0;
+  for (int i = 1; i < 4; i++)
+    if (sum[i] > sum[top]) top = i;
+  if (total_ms) *total_ms = sum[top];
+  if (launches) *launches = cnt[top];
   return rc;
 }
 
@@ -355,7 +366,7 @@ int ffd_cdist(const void* setA, int64_t nA, int32_t lenA, const void* setB, int6
   a.out = out;
   a.ld_out = ld_out;
   a.workspace = workspace;
-  ProfScope prof(reinterpret_cast<cudaStream_t>(stream));
+  ProfScope prof(reinterpret_cast<cudaStream_t>(stream), 3);
   return launch_cdist(a, dev_info().sms, reinterpret_cast<cudaStream_t>(stream), &g_launches);
 }
 

@@ -1,0 +1,9 @@
+// longpair_d2.cu — long-pair kernel instantiations for D = 2 (one TU per
+// dimension so the build runs them in parallel).
+#include "longpair_kernel.cuh"
+
+namespace ffd {
+cudaError_t launch_long_dim2(const LongArgs& a, int sms, cudaStream_t st, const LongWs& w, int G) {
+  return launch_long_dim<2>(a, sms, st, w, G);
+}
+}  // namespace ffd

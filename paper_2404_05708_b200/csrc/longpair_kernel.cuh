@@ -1,0 +1,413 @@
+// longpair_kernel.cuh — one very long pair spread over the whole GPU
+// (BASELINE config 5).
+//
+// What: δ_dF of a pair with n rows (the shorter curve) and m columns, Eq. (1)
+// in linear memory (Theorem 1): every warp keeps only
+// its strip of rows and one column of DP state in registers.
+//
+// How:
+//   * The rows are cut into bands of 32·R rows; band b runs on one warp as the
+//     lane-strip wavefront of strip.cuh (lane ℓ: rows [ℓR, ℓR+R), column t−ℓ at
+//     step t) and streams all m columns once.
+//   * Band b's bottom row (lane 31's value, one per column) is band b+1's top
+//     input.  It moves through LINKS: rings of 8-byte slots {value, tag} written
+//     by lane 31 with one 64-bit store, tag = absolute stream position + 1.  The
+//     consumer polls the slot itself, so data and "ready" arrive together and no
+//     fence or flag is needed (the low-latency protocol NCCL calls LL).  Inside
+//     a CTA the ring is in shared memory; between CTAs (warp 7 → next CTA's
+//     warp 0) it is in global memory (L2).
+//   * The consumer prefetches the slots of the next 32 columns one chunk ahead
+//     (like the column points), checks the tags when it stores them into its
+//     column ring, and re-polls only the slots that were not ready.  It
+//     publishes how far it has consumed; the producer checks that counter (also
+//     prefetched) before reusing slots: bounded rings, no overwrite.
+//   * One persistent CTA of 8 warps per SM, cooperative launch: all bands are
+//     co-resident, so spinning on a neighbour cannot deadlock.  Counters and
+//     tags are absolute positions, so successive long pairs need no grid barrier.
+#pragma once
+#include <climits>
+
+#include "longpair.cuh"
+#include "strip.cuh"
+
+namespace ffd {
+
+constexpr int kLWarps = 8;          // warps (bands) per CTA
+constexpr int kLSmemRing = 128;     // slots per intra-CTA link
+constexpr int kLGlobRing = 2048;    // slots per inter-CTA link
+constexpr int kMaxLongCtas = 1024;
+
+struct LongProblem {
+  const void* p;
+  const void* q;
+  const int64_t* offsets;
+  const int32_t* lengths;
+  int64_t num_pairs;
+  const int* list;
+  const int* list_count;
+  void* out;
+  uint2* gring;    // [G][kLGlobRing] slots of the link CTA g → g+1 (zeroed per call)
+  unsigned* gcons; // [G] consumer progress on the link CTA g → g+1 (zeroed per call)
+  int* bad;        // per long pair: a point left the fp32-exact window (int input)
+};
+
+__device__ __forceinline__ uint2 ld_slot(const uint2* p) {
+  uint2 v;
+  asm volatile("ld.volatile.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_slot(uint2* p, float v, unsigned tag) {
+  asm volatile("st.volatile.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(__float_as_uint(v)), "r"(tag)
+               : "memory");
+}
+__device__ __forceinline__ unsigned ld_ctr(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.volatile.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_ctr(unsigned* p, unsigned v) {
+  asm volatile("st.volatile.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// one link endpoint: ring of slots (mask = size − 1) and the consumer counter
+struct Link {
+  uint2* ring;
+  unsigned mask;
+  unsigned* cons;
+};
+
+template <int KIND, int D, bool INT_IN, int FIN, int R>
+struct LongRunner {
+  using T = float;
+  using C = SCfg<T, KIND, D, INT_IN>;
+  using In = typename std::conditional<INT_IN, int32_t, float>::type;
+  static constexpr int NS = C::NS;
+
+  uint4* ring;  // this warp's column ring [kRing * EW]
+  const LongProblem& pb;
+  int lane;
+
+  // ---- pair description --------------------------------------------------
+  const In* rows;
+  const In* cols;
+  int n, m;
+  int center[D];
+
+  __device__ bool conv(const In (&a)[D], float (&v)[D]) const {
+    bool ok = true;
+#pragma unroll
+    for (int c = 0; c < D; c++) {
+      if constexpr (INT_IN) {
+        long long t = (long long)a[c] - center[c];
+        ok &= (t >= -C::LIM) && (t <= C::LIM);
+        v[c] = (float)(int)t;
+      } else {
+        v[c] = a[c];
+      }
+    }
+    return ok;
+  }
+
+  // column element of position `pos` (0 = sentinel), written with its top value
+  __device__ void store_elem(const In (&a)[D], int kind, int pos, float top, bool& ok) {
+    alignas(16) float f[C::EBYTES / 4];
+#pragma unroll
+    for (int i = 0; i < C::EBYTES / 4; i++) f[i] = 0.f;
+    if (kind != 0) {
+      if constexpr (C::XSQ) {
+        f[D] = finf();
+      } else {
+#pragma unroll
+        for (int c = 0; c < D; c++) f[c] = finf();
+      }
+    } else {
+      float v[D];
+      ok &= conv(a, v);
+      if constexpr (C::XSQ) {
+        int qq = 0;
+#pragma unroll
+        for (int c = 0; c < D; c++) {
+          qq += (int)v[c] * (int)v[c];
+          f[c] = -2.f * v[c];
+        }
+        f[D] = (float)qq;
+      } else {
+#pragma unroll
+        for (int c = 0; c < D; c++) f[c] = v[c];
+      }
+    }
+    f[C::I_TOP] = top;
+    uint4* dst = ring + (pos & kRingMask) * C::EW;
+#pragma unroll
+    for (int w = 0; w < C::EW; w++) dst[w] = reinterpret_cast<const uint4*>(f)[w];
+  }
+
+  __device__ void fetch(int pos, int S, In (&a)[D], int& kind) const {
+#pragma unroll
+    for (int c = 0; c < D; c++) a[c] = (In)0;
+    if (pos >= S) {
+      kind = 2;
+    } else if (pos == 0) {
+      kind = 1;
+    } else {
+      kind = 0;
+#pragma unroll
+      for (int c = 0; c < D; c++) a[c] = __ldg(cols + (int64_t)(pos - 1) * D + c);
+    }
+  }
+
+  // top value of position `pos` for this band: the corner/border for band 0,
+  // else the producer's slot (spinning until its tag shows up)
+  __device__ __forceinline__ float top_of(int pos, int S, bool has_in, const Link& in, unsigned tb,
+                                          uint2 pre) const {
+    if (pos >= S) return finf();
+    if (!has_in) return pos == 0 ? 0.f : finf();
+    const unsigned want = tb + (unsigned)pos + 1u;
+    while (pre.y != want) pre = ld_slot(in.ring + ((unsigned)pos & in.mask));
+    return __uint_as_float(pre.x);
+  }
+
+  // one band of 32·R rows starting at row r0
+  __device__ bool run_band(int r0, bool has_in, Link in, bool has_out, Link out, bool last_band,
+                           int out_idx, int* bad_flag, unsigned tb) {
+    const int S = m + 1;
+    bool ok = true;
+    float x[NS][R], c[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      const int row = min(r0 + lane * R + r, n - 1);
+      In a[D];
+#pragma unroll
+      for (int cc = 0; cc < D; cc++) a[cc] = __ldg(rows + (int64_t)row * D + cc);
+      float v[D];
+      ok &= conv(a, v);
+#pragma unroll
+      for (int cc = 0; cc < D; cc++) x[cc][r] = v[cc];
+      if constexpr (C::XSQ) {
+        int pp = 0;
+#pragma unroll
+        for (int cc = 0; cc < D; cc++) pp += (int)v[cc] * (int)v[cc];
+        x[D][r] = (float)pp;
+      }
+      c[r] = finf();
+    }
+    if constexpr (INT_IN) {
+      if (!__all_sync(0xffffffffu, ok) && lane == 0) atomicExch(bad_flag, 1);
+    }
+    float diag = finf();
+    const uint2 none = make_uint2(0u, 0u);
+    // prologue: positions [0, 32) stored, [32, 64) prefetched
+    In a[D];
+    int kind;
+    fetch(lane, S, a, kind);
+    uint2 pre = (has_in && lane < S) ? ld_slot(in.ring + ((unsigned)lane & in.mask)) : none;
+    store_elem(a, kind, lane, top_of(lane, S, has_in, in, tb, pre), ok);
+    fetch(32 + lane, S, a, kind);
+    pre = (has_in && 32 + lane < S) ? ld_slot(in.ring + ((unsigned)(32 + lane) & in.mask)) : none;
+    __syncwarp();
+    if (has_in && lane == 0) st_ctr(in.cons, tb + (unsigned)min(32, S));
+    unsigned cons_seen = 0, cons_next = 0;
+    if (has_out) cons_seen = cons_next = ld_ctr(out.cons);
+
+    const int total = S + 31;
+    int t = 0, next_refill = 32;
+    while (t < total) {
+      if (t == next_refill) {
+        store_elem(a, kind, t + lane, top_of(t + lane, S, has_in, in, tb, pre), ok);
+        fetch(t + 32 + lane, S, a, kind);
+        const int pn = t + 32 + lane;
+        pre = (has_in && pn < S) ? ld_slot(in.ring + ((unsigned)pn & in.mask)) : none;
+        __syncwarp();
+        if (has_in && lane == 0) st_ctr(in.cons, tb + (unsigned)min(t + 32, S));
+        next_refill += 32;
+      }
+      if (has_out) {
+        // lane 31 writes positions ≤ t during the next 32 steps: their slots must be
+        // consumed (cons + ring > tb + t).  The counter is read one chunk ahead.
+        if (lane == kWarp - 1 && (t & 31) == 0) {
+          cons_seen = cons_next;
+          while ((int)(cons_seen + out.mask + 1u - (tb + (unsigned)t)) <= 0) cons_seen = ld_ctr(out.cons);
+          cons_next = ld_ctr(out.cons);
+        }
+      }
+      __syncwarp();
+      const int stop = min(next_refill, total);
+      int g = t - lane;
+      if (has_out) {
+#pragma unroll 1
+        for (; t < stop; ++t, ++g) {
+          warp_step<float, KIND, D, R, INT_IN>(c, diag, x, ring, g, lane);
+          if (lane == kWarp - 1 && g >= 0 && g < S)
+            st_slot(out.ring + ((unsigned)g & out.mask), c[R - 1], tb + (unsigned)g + 1u);
+        }
+      } else {
+#pragma unroll 1
+        for (; t + 2 <= stop; t += 2, g += 2) {
+          warp_step<float, KIND, D, R, INT_IN>(c, diag, x, ring, g, lane);
+          warp_step<float, KIND, D, R, INT_IN>(c, diag, x, ring, g + 1, lane);
+        }
+        if (t < stop) {
+          warp_step<float, KIND, D, R, INT_IN>(c, diag, x, ring, g, lane);
+          ++t;
+        }
+      }
+    }
+    const bool all_ok = __all_sync(0xffffffffu, ok);
+    if (last_band && lane == kWarp - 1) {
+      if constexpr (INT_IN) {
+        __threadfence();
+        const bool bad = !all_ok || *reinterpret_cast<volatile int*>(bad_flag) != 0;
+        reinterpret_cast<long long*>(pb.out)[out_idx] = bad ? LLONG_MIN : (long long)c[R - 1];
+      } else {
+        float f = c[R - 1];
+        if constexpr (FIN == F_SQRT) f = __fsqrt_rn(f);
+        reinterpret_cast<float*>(pb.out)[out_idx] = f;
+      }
+    }
+    __syncwarp();
+    return all_ok;
+  }
+};
+
+// rows per lane for a pair with n rows on G co-resident CTAs: the smallest
+// built R whose bands all fit at once (⌈bands / 8⌉ ≤ G); 0 if none does
+__host__ __device__ inline int long_rows_per_lane(int n, int G) {
+  const int rs[5] = {4, 7, 8, 16, 32};  // the R the long kernel is built for
+  for (int i = 0; i < 5; i++) {
+    const int R = rs[i];
+    const int nb = (n + kWarp * R - 1) / (kWarp * R);
+    if ((nb + kLWarps - 1) / kLWarps <= G) return R;
+  }
+  return 0;
+}
+
+template <int KIND, int D, bool INT_IN, int FIN>
+__global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProblem pb) {
+  using C = SCfg<float, KIND, D, INT_IN>;
+  using In = typename std::conditional<INT_IN, int32_t, float>::type;
+  __shared__ uint4 rings[kLWarps][kRing * C::EW];
+  __shared__ uint2 slink[kLWarps][kLSmemRing];
+  __shared__ unsigned scons[kLWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x, cta = blockIdx.x;
+  for (int i = threadIdx.x; i < kLWarps * kLSmemRing; i += blockDim.x)
+    (&slink[0][0])[i] = make_uint2(0u, 0u);
+  if (threadIdx.x < kLWarps) scons[threadIdx.x] = 0u;
+  __syncthreads();
+  const int npairs = *pb.list_count;
+  unsigned tb = 0;  // tag base: absolute stream position of the current pair on every link
+  for (int li = 0; li < npairs; li++) {
+    const int k = pb.list[li];
+    const int64_t B = pb.num_pairs;
+    const int n0 = pb.lengths[k], m0 = pb.lengths[B + k];
+    const bool swap = n0 > m0;
+    const int n = swap ? m0 : n0, m = swap ? n0 : m0;
+    const In* rows = reinterpret_cast<const In*>(swap ? pb.q : pb.p) +
+                     (swap ? pb.offsets[B + k] : pb.offsets[k]) * D;
+    const In* cols = reinterpret_cast<const In*>(swap ? pb.p : pb.q) +
+                     (swap ? pb.offsets[k] : pb.offsets[B + k]) * D;
+    const int R = long_rows_per_lane(n, G);
+    const int S = m + 1;
+    if (R == 0) {
+      if (cta == 0 && threadIdx.x == 0) {
+        if constexpr (INT_IN) reinterpret_cast<long long*>(pb.out)[k] = LLONG_MIN;
+        else reinterpret_cast<float*>(pb.out)[k] = __int_as_float(0x7fc00000);
+      }
+      continue;
+    }
+    const int band_rows = kWarp * R;
+    const int nb = (n + band_rows - 1) / band_rows;
+    const int b = cta * kLWarps + warp;
+    if (!(b < nb && b > 0) && lane == 0) {
+      // this warp does not consume its input link for this pair: its producer
+      // (if any) writes nothing of it either, so mark the whole stream consumed —
+      // otherwise the producer of a later pair would wait on a stale counter
+      unsigned* cons = (warp > 0) ? &scons[warp - 1] : pb.gcons + (cta + G - 1) % G;
+      st_ctr(cons, tb + (unsigned)S);
+    }
+    if (b < nb) {
+      const bool has_in = b > 0, has_out = b + 1 < nb;
+      Link in{}, out{};
+      if (warp > 0) {
+        in = Link{slink[warp - 1], kLSmemRing - 1u, &scons[warp - 1]};
+      } else {
+        const int src = (cta + G - 1) % G;
+        in = Link{pb.gring + (size_t)src * kLGlobRing, kLGlobRing - 1u, pb.gcons + src};
+      }
+      if (warp < kLWarps - 1) out = Link{slink[warp], kLSmemRing - 1u, &scons[warp]};
+      else out = Link{pb.gring + (size_t)cta * kLGlobRing, kLGlobRing - 1u, pb.gcons + cta};
+      auto go = [&](auto& run) {
+        run.n = n;
+        run.m = m;
+        run.rows = rows;
+        run.cols = cols;
+        if constexpr (INT_IN) {
+#pragma unroll
+          for (int c = 0; c < D; c++) run.center[c] = (int)rows[c];
+        }
+        run.run_band(b * band_rows, has_in, in, has_out, out, b == nb - 1, k, pb.bad + li, tb);
+      };
+      if (R == 4) {
+        LongRunner<KIND, D, INT_IN, FIN, 4> run{rings[warp], pb, lane};
+        go(run);
+      } else if (R == 7) {
+        LongRunner<KIND, D, INT_IN, FIN, 7> run{rings[warp], pb, lane};
+        go(run);
+      } else if (R == 8) {
+        LongRunner<KIND, D, INT_IN, FIN, 8> run{rings[warp], pb, lane};
+        go(run);
+      } else if (R == 16) {
+        LongRunner<KIND, D, INT_IN, FIN, 16> run{rings[warp], pb, lane};
+        go(run);
+      } else {
+        LongRunner<KIND, D, INT_IN, FIN, 32> run{rings[warp], pb, lane};
+        go(run);
+      }
+    }
+    __syncthreads();
+    tb += (unsigned)S;  // every link's absolute position advances by one stream per pair
+  }
+}
+
+struct LongWs {
+  uint2* gring;
+  unsigned* gcons;
+  int* bad;
+};
+
+// One persistent CTA (8 bands) per SM, cooperative launch.  BASELINE config 5
+// (n = 262,144) runs as 147 CTAs of 8 bands × 224 rows (R = 7).
+template <int KIND, int D, bool INT_IN, int FIN>
+cudaError_t launch_long_k(const LongArgs& a, int sms, cudaStream_t st, const LongWs& w, int G) {
+  auto k = long_kernel<KIND, D, INT_IN, FIN>;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kWarp * kLWarps, 0);
+  if (occ < 1) return cudaErrorLaunchOutOfResources;
+  if (G > sms * occ) G = sms * occ;
+  LongProblem pb{a.p,      a.q,       a.offsets, a.lengths, a.num_pairs, a.list,
+                 a.list_count, a.out, w.gring,   w.gcons,   w.bad};
+  void* args[] = {&pb};
+  return cudaLaunchCooperativeKernel((const void*)k, dim3(G), dim3(kWarp * kLWarps), args, 0, st);
+}
+
+// per-dimension dispatch (longpair_d<D>.cu)
+cudaError_t launch_long_dim1(const LongArgs& a, int sms, cudaStream_t st, const LongWs& w, int G);
+cudaError_t launch_long_dim2(const LongArgs& a, int sms, cudaStream_t st, const LongWs& w, int G);
+cudaError_t launch_long_dim3(const LongArgs& a, int sms, cudaStream_t st, const LongWs& w, int G);
+cudaError_t launch_long_dim4(const LongArgs& a, int sms, cudaStream_t st, const LongWs& w, int G);
+
+template <int D>
+cudaError_t launch_long_dim(const LongArgs& a, int sms, cudaStream_t st, const LongWs& w, int G) {
+  const bool i = a.dtype == 1;
+  if (!i) {
+    if (a.norm == 1) return launch_long_k<K_L1, D, false, F_NONE>(a, sms, st, w, G);
+    if (a.norm == 3) return launch_long_k<K_LINF, D, false, F_NONE>(a, sms, st, w, G);
+    if (a.norm == 2) return launch_long_k<K_SQ, D, false, F_SQRT>(a, sms, st, w, G);
+    return launch_long_k<K_SQ, D, false, F_NONE>(a, sms, st, w, G);
+  }
+  if (a.norm == 4) return launch_long_k<K_XSQ, D, true, F_NONE>(a, sms, st, w, G);
+  if (a.norm == 1) return launch_long_k<K_L1, D, true, F_NONE>(a, sms, st, w, G);
+  return launch_long_k<K_LINF, D, true, F_NONE>(a, sms, st, w, G);
+}
+
+}  // namespace ffd

@@ -197,3 +197,49 @@ def test_batch_host_matches_device(ffd):
     dev = ffd.batch(*to_dev(b), norm="sql2").cpu().numpy()
     host = ffd.batch_host(b.p, b.q, b.offsets, b.lengths, norm="sql2")
     assert np.array_equal(dev, host)
+
+
+def test_config2_full_size_exact(ffd):
+    """Full BASELINE config 2 (100k pairs, lengths U[128,512], int32 sq-L2) in the
+    launch configuration bench.py times: every pair bit-exact against the int64 oracle."""
+    b = workload.gen_batch(workload.CONFIGS[2])
+    out = ffd.batch(*to_dev(b), norm="sql2")
+    check_int(out.cpu().numpy(), b, "sql2")
+
+
+def test_config3_full_size_sampled(ffd):
+    """Full BASELINE config 3 (1M pairs, 3-D fp32, lengths U[256,1024], ≈15 GB of
+    points) in the bench launch shape; 3000 seeded pairs checked one by one against
+    the fp64 oracle (≤ 1e-5) and the fp32 mirror (bit-exact); every output finite."""
+    cfg = workload.CONFIGS[3]
+    b = workload.gen_batch(cfg)
+    out = ffd.batch(*to_dev(b), norm="l2").cpu().numpy()
+    assert np.isfinite(out).all() and (out >= 0).all()
+    B = b.num_pairs
+    idx = np.unique(workload.sample_indices(cfg, 0, 3000, B))
+    sel = [(b.p[b.offsets[k]: b.offsets[k] + b.lengths[k]],
+            b.q[b.offsets[B + k]: b.offsets[B + k] + b.lengths[B + k]]) for k in idx]
+    lp = np.array([len(p) for p, _ in sel], np.int32)
+    lq = np.array([len(q) for _, q in sel], np.int32)
+    sub = workload.Batch(np.concatenate([p for p, _ in sel]), np.concatenate([q for _, q in sel]),
+                         np.concatenate([np.concatenate([[0], np.cumsum(lp)[:-1]]),
+                                         np.concatenate([[0], np.cumsum(lq)[:-1]])]).astype(np.int64),
+                         np.concatenate([lp, lq]), 3, "l2")
+    check_float(out[idx], sub, "l2")
+
+
+@pytest.mark.parametrize("norm", ["l2", "l1"])
+def test_odd_even_columns_and_bands(ffd, norm):
+    """Column counts of both parities (the stream repeats the last column of pairs
+    with an odd m + 1) across every band shape: 1..4 bands, R at its extremes."""
+    rng = np.random.default_rng(77)
+    rows = [1, 2, 31, 32, 33, 63, 64, 65, 511, 512, 513, 1023, 1024, 1025, 2047, 2048]
+    lens = []
+    for n in rows:
+        for m in (n, n + 1, n + 2, 2000, 2001):
+            lens.append((n, m))
+    lens = np.array(lens, np.int32)
+    L = np.concatenate([lens[:, 0], lens[:, 1]]).astype(np.int32)
+    b = make_batch(rng, len(lens), 0, 0, lens=L)
+    out = ffd.batch(*to_dev(b), norm=norm)
+    check_float(out.cpu().numpy(), b, norm)

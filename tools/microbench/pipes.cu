@@ -71,6 +71,68 @@ __global__ void op_kernel(float* out, long long* cyc, int iters) {
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
+
+// ---- mixed independent streams: do two op types share one pipe? ----------
+// MIX 0: FFMA2+FMNMX3  1: FFMA2+FMNMX  2: FFMA+FMNMX  3: FADD2+FFMA2+FMNMX3+FMNMX
+// (the fp32 2-D cell mix, 7 slots on one shared pipe)  4: FADD2+2 FFMA2+2 FMNMX3+
+// 2 FMNMX (two exact-int XSQ cells, 12 slots)  5: FMNMX3+FMNMX  6: FFMA2+IADD3
+// 7: FMNMX3+IADD3.  instr_per_unit is the number of instructions per chain unit.
+template <int MIX>
+__global__ void mix_kernel(float* out, long long* cyc, int iters) {
+  float a[NCHAIN], b[NCHAIN];
+  int ia[NCHAIN];
+  uint64_t p[NCHAIN], q[NCHAIN];
+  float y = 1.0001f + threadIdx.x * 1e-7f, z = 0.9999f - threadIdx.x * 1e-7f;
+  int yi = threadIdx.x | 1;
+  uint64_t y2 = pack(y, z), z2 = pack(z, y);
+#pragma unroll
+  for (int u = 0; u < NCHAIN; u++) {
+    a[u] = threadIdx.x * 0.001f + u;
+    b[u] = threadIdx.x * 0.002f - u;
+    ia[u] = threadIdx.x * 3 + u;
+    p[u] = pack(a[u], a[u] + 1.f);
+    q[u] = pack(b[u], b[u] + 2.f);
+  }
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int r = 0; r < UNROLL; r++) {
+#pragma unroll
+      for (int u = 0; u < NCHAIN; u++) {
+        if (MIX == 0 || MIX == 1 || MIX == 3 || MIX == 4 || MIX == 6)
+          asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(p[u]) : "l"(y2), "l"(z2));
+        if (MIX == 3 || MIX == 4)
+          asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(q[u]) : "l"(y2));
+        if (MIX == 4)
+          asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(q[u]) : "l"(z2), "l"(y2));
+        if (MIX == 2) asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(b[u]) : "f"(y), "f"(z));
+        if (MIX == 0 || MIX == 3 || MIX == 4 || MIX == 5 || MIX == 7) {
+          float t;
+          asm volatile("min.f32 %0, %1, %2;\n\tmin.f32 %0, %0, %3;" : "=f"(t) : "f"(a[u]), "f"(y), "f"(z));
+          a[u] = t;
+        }
+        if (MIX == 4) {
+          float t;
+          asm volatile("min.f32 %0, %1, %2;\n\tmin.f32 %0, %0, %3;" : "=f"(t) : "f"(b[u]), "f"(z), "f"(y));
+          b[u] = t;
+        }
+        if (MIX == 1 || MIX == 2 || MIX == 3 || MIX == 4 || MIX == 5)
+          asm volatile("max.f32 %0, %0, %1;" : "+f"(b[u]) : "f"(y));
+        if (MIX == 4) asm volatile("max.f32 %0, %0, %1;" : "+f"(a[u]) : "f"(z));
+        if (MIX == 6 || MIX == 7) asm volatile("add.s32 %0, %0, %1;" : "+r"(ia[u]) : "r"(yi));
+      }
+    }
+  }
+  long long t1 = clock64();
+  float s = 0.f;
+#pragma unroll
+  for (int u = 0; u < NCHAIN; u++)
+    s += a[u] + b[u] + (float)ia[u] + __uint_as_float((uint32_t)p[u]) + __uint_as_float((uint32_t)q[u]);
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
 // ---- cell tests: R rows in registers, one column per step ------------------
 // q comes from a shared-memory ring (one LDS.128 per step, as in the real
 // kernel); SHF=1 adds the lane-to-lane __shfl_up_sync of the real pipeline.
@@ -223,6 +285,15 @@ int main() {
   run(names[11], op_kernel<11>, 4, 256, IT, per, "warp-instr");
   run(names[12], op_kernel<12>, 4, 256, IT, per, "warp-instr");
   run(names[13], op_kernel<13>, 4, 256, IT / 4, per, "warp-instr");
+  // mixed streams (warp-instructions of all kinds per clock per SM)
+  run("mix_FFMA2+FMNMX3", mix_kernel<0>, 4, 256, IT, per * 2, "warp-instr");
+  run("mix_FFMA2+FMNMX", mix_kernel<1>, 4, 256, IT, per * 2, "warp-instr");
+  run("mix_FFMA+FMNMX", mix_kernel<2>, 4, 256, IT, per * 2, "warp-instr");
+  run("mix_cell_f32_FADD2+FFMA2+FMNMX3+FMNMX", mix_kernel<3>, 4, 256, IT, per * 4, "warp-instr");
+  run("mix_cell_xsq_2cells_FADD2+2FFMA2+2FMNMX3+2FMNMX", mix_kernel<4>, 4, 256, IT, per * 7, "warp-instr");
+  run("mix_FMNMX3+FMNMX", mix_kernel<5>, 4, 256, IT, per * 2, "warp-instr");
+  run("mix_FFMA2+IADD3", mix_kernel<6>, 4, 256, IT, per * 2, "warp-instr");
+  run("mix_FMNMX3+IADD3", mix_kernel<7>, 4, 256, IT, per * 2, "warp-instr");
   // cells per clock per SM: per thread-step = R cells; lanes x warps
   const int ST = 4000;
   int wl[3] = {8, 16, 32};

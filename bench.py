@@ -31,9 +31,33 @@ import workload  # noqa: E402
 METRIC = "DP cells/sec (G cells/s) batched & all-pairs Fréchet; % of ALU roofline"
 UNIT = "Gcells/s"
 SM_MAX_MHZ_NOMINAL = 1965.0
-# ALU roofline: 148 SMs × 4 SMSPs × 32 lanes = 128 lane-ops/clk/SM of the
-# FP32/INT pipe; cells/s = 148·128·f / ops_per_cell, ops_per_cell = minimal SASS pipe-ops per cell.
-OPS_PER_CELL = {1: 7, 2: 6, 3: 9, 4: 7, 5: 7}
+# ALU roofline: peak cells/s = SMs × f_max × C, where C (cells per clock per SM) is
+# the MEASURED throughput of the cell's minimal SASS instruction mix run as independent chains at
+# 32 warps/SM (tools/microbench/pipes.cu `mixcells_*`, profiles/r1_microbench_pipes_v2.jsonl).  The
+# FMA pipe (FADD2/FFMA2/FMUL2) and the ALU pipe (FMNMX3/FMNMX) overlap, so this is above a
+# one-pipe count.  ISSUE_PER_CELL is the instruction count of that mix per warp-cell-row (issue
+# bound: 4 SMSPs × 1 instr/clk), reported beside it as the looser ceiling.
+MIX_CELLS_PER_CLK = {"f32_d2_sq": 29.683, "xsq_d2": 24.909, "f32_d3_sq": 16.592,
+                     "f32_d2_l1": 25.966, "f32_d2_linf": 22.754}
+ISSUE_PER_CELL = {"f32_d2_sq": 4.0, "xsq_d2": 3.5, "f32_d3_sq": 5.0, "f32_d2_l1": 4.0,
+                  "f32_d2_linf": 3.0}
+CELL_OF_CONFIG = {1: "f32_d2_sq", 2: "xsq_d2", 3: "f32_d3_sq", 4: "f32_d2_sq", 5: "f32_d2_sq"}
+CELL_OF_NORM = {"l1": "f32_d2_l1", "l2": "f32_d2_sq", "linf": "f32_d2_linf"}
+MIX_SOURCE = "profiles/r1_microbench_pipes_v2.jsonl (tools/microbench/pipes.cu mixcells_*)"
+
+
+def alu_roofline(cells_per_launch, kernel_ms, cell, sms, f_max, f_meas, kernel, traffic):
+    """The roofline object for the dominant kernel."""
+    achieved = cells_per_launch / (kernel_ms * 1e-3) / 1e9
+    c = MIX_CELLS_PER_CLK[cell]
+    peak = sms * c * f_max / 1e9
+    issue_peak = sms * 128.0 / ISSUE_PER_CELL[cell] * f_max / 1e9
+    return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": UNIT, "frac": achieved / peak,
+            "traffic": traffic, "kernel": kernel, "kernel_ms": kernel_ms, "cell": cell,
+            "peak_basis": f"{sms} SMs x {c} cells/clk/SM (measured mix of the cell's SASS ops, {MIX_SOURCE})"
+                          f" x {f_max/1e6:.0f} MHz (max SM clock)",
+            "frac_at_measured_clock": achieved / (sms * c * f_meas / 1e9),
+            "issue_bound_peak": issue_peak, "frac_of_issue_bound": achieved / issue_peak}
 
 
 def dist_env():
@@ -304,18 +328,10 @@ def bench_ffd(args):
     clocks = sampler.summary()
     f_meas = (clocks["sm_mhz"] or SM_MAX_MHZ_NOMINAL) * 1e6
     f_max = (clocks["sm_max_mhz"] or SM_MAX_MHZ_NOMINAL) * 1e6
-    ops = OPS_PER_CELL[cfg.cid]
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    peak = sms * 128 * f_max / ops / 1e9
-    achieved = cells / (kern_ms * 1e-3) / 1e9
-    roofline = {
-        "bound": "alu", "achieved": achieved, "peak": peak, "unit": UNIT,
-        "frac": achieved / peak, "traffic": args.traffic,
-        "kernel": "batch_kernel (fp32-exact int sqL2 cell)", "kernel_ms": kern_ms,
-        "ops_per_cell": ops,
-        "peak_basis": f"{sms} SMs x 128 lane-ops/clk x {f_max/1e6:.0f} MHz (max clock) / {ops} ops per cell",
-        "frac_at_measured_clock": achieved / (sms * 128 * f_meas / ops / 1e9),
-    }
+    cell = CELL_OF_CONFIG[cfg.cid]
+    roofline = alu_roofline(cells, kern_ms, cell, sms, f_max, f_meas,
+                            f"batch_kernel ({cell} cell)", args.traffic)
 
     cpu = cpu_baseline_line(args, cfg, ws)
 
@@ -431,9 +447,6 @@ def bench_cdist(args):
         f_max = (clocks["sm_max_mhz"] or SM_MAX_MHZ_NOMINAL) * 1e6
         f_meas = (clocks["sm_mhz"] or SM_MAX_MHZ_NOMINAL) * 1e6
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        ops = OPS_PER_CELL[4]
-        peak = sms * 128 * f_max / ops / 1e9
-        ach = cells_rank / (kern_ms * 1e-3) / 1e9
         line = {
             "metric": METRIC, "value": total_cells / (ms_max * 1e-3) / 1e9, "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
@@ -444,11 +457,8 @@ def bench_cdist(args):
                        "l2": "B (20 MB) L2-resident by design; output 1.6 GB streamed"},
             "clocks": clocks,
             "cpu_baseline": cpu_baseline_line(args, cfg, ws),
-            "roofline": {"bound": "alu", "achieved": ach, "peak": peak, "unit": UNIT, "frac": ach / peak,
-                         "traffic": args.traffic, "kernel": "cdist_kernel (fp32 L2, W=8 R=16)",
-                         "kernel_ms": kern_max, "ops_per_cell": ops,
-                         "peak_basis": f"{sms} SMs x 128 lane-ops/clk x {f_max/1e6:.0f} MHz / {ops} ops per cell",
-                         "frac_at_measured_clock": ach / (sms * 128 * f_meas / ops / 1e9)},
+            "roofline": alu_roofline(cells_rank, kern_max, CELL_OF_CONFIG[4], sms, f_max, f_meas,
+                                     "cdist_kernel (fp32 L2, W=8 R=16)", args.traffic),
             "e2e": {"value": total_cells / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": A_h.nbytes + B_h.nbytes,
                     "d2h_bytes_per_step": cfg.nA * cfg.nB * 4},
@@ -500,20 +510,24 @@ def bench_long(args):
         dist.barrier()
     torch.cuda.synchronize()
     sampler = ClockSampler(dev.index)
-    per_norm = {nm: 0.0 for nm in cfg.norms}
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with sampler:
         e0.record(stream)
         for _ in range(args.steps):
-            for nm in cfg.norms:
-                ffd.profile_enable(True)
-                ffd.batch(p, q, off, lens, norm=nm, out=outs[nm])
-                ffd.profile_enable(False)
-                per_norm[nm] += ffd.profile_take()[0]
+            step()
         e1.record(stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
     launches = ffd.launches_taken() // args.steps
+    # per-norm duration of the dominant (long-pair) kernel: a second, instrumented pass
+    per_norm = {nm: 0.0 for nm in cfg.norms}
+    for _ in range(args.steps):
+        for nm in cfg.norms:
+            ffd.profile_enable(True)
+            ffd.batch(p, q, off, lens, norm=nm, out=outs[nm])
+            ffd.profile_enable(False)
+            per_norm[nm] += ffd.profile_take()[0]
+    ffd.launches_taken()
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -538,10 +552,9 @@ def bench_long(args):
         f_max = (clocks["sm_max_mhz"] or SM_MAX_MHZ_NOMINAL) * 1e6
         f_meas = (clocks["sm_mhz"] or SM_MAX_MHZ_NOMINAL) * 1e6
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        ops = OPS_LONG
         kern = {nm: per_norm[nm] / args.steps for nm in cfg.norms}
-        ach = {nm: cells / (kern[nm] * 1e-3) / 1e9 for nm in cfg.norms}
-        peak = {nm: sms * 128 * f_max / ops[nm] / 1e9 for nm in cfg.norms}
+        per = {nm: alu_roofline(cells, kern[nm], CELL_OF_NORM[nm], sms, f_max, f_meas,
+                                f"long_kernel (fp32 {nm})", args.traffic) for nm in cfg.norms}
         line = {
             "metric": METRIC, "value": ws * 3 * cells / (ms_max * 1e-3) / 1e9, "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
@@ -551,13 +564,9 @@ def bench_long(args):
                        "l2": "inputs 4.2 MB (L2-resident); the DP state never leaves the SMs"},
             "clocks": clocks,
             "cpu_baseline": cpu_baseline_line(args, cfg, ws),
-            "roofline": {"bound": "alu", "achieved": ach["l2"], "peak": peak["l2"], "unit": UNIT,
-                         "frac": ach["l2"] / peak["l2"], "traffic": args.traffic,
-                         "kernel": "long_kernel (fp32 L2)", "kernel_ms": kern["l2"], "ops_per_cell": ops["l2"],
-                         "per_norm": {nm: {"kernel_ms": kern[nm], "achieved": ach[nm], "peak": peak[nm],
-                                           "frac": ach[nm] / peak[nm], "ops_per_cell": ops[nm]}
-                                      for nm in cfg.norms},
-                         "frac_at_measured_clock": ach["l2"] / (sms * 128 * f_meas / ops["l2"] / 1e9)},
+            "roofline": dict(per["l2"], per_norm={nm: {k: per[nm][k] for k in
+                                                        ("kernel_ms", "achieved", "peak", "frac", "cell")}
+                                                   for nm in cfg.norms}),
             "e2e": {"value": ws * 3 * cells / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": p_h.nbytes + q_h.nbytes, "d2h_bytes_per_step": 4 * len(cfg.norms)},
             "results": vals,
@@ -567,12 +576,6 @@ def bench_long(args):
     if ws > 1:
         dist.destroy_process_group()
     return 0
-
-
-# slots per cell of the minimal fp32 D=2 cell per norm: L1 = 2 (FSUB2)
-# + 1 (FADD |a|+|b|) + 2 (FMNMX3) + 1 (FMNMX); L2 = 7; L∞ = 2 (FSUB2) + 1 (FMNMX |a|,|b|)
-# + 2 + 1
-OPS_LONG = {"l1": 6, "l2": 7, "linf": 6}
 
 
 def main():

@@ -26,6 +26,7 @@
 //     tags are absolute positions, so successive long pairs need no grid barrier.
 #pragma once
 #include <climits>
+#include <cstdio>
 
 #include "longpair.cuh"
 #include "strip.cuh"
@@ -33,9 +34,13 @@
 namespace ffd {
 
 constexpr int kLWarps = 8;          // warps (bands) per CTA
-constexpr int kLSmemRing = 128;     // slots per intra-CTA link
+constexpr int kLSmemRing = 1024;    // slots per intra-CTA link (8 KB; the producer may run
+                                    // ~500 steps ahead, far beyond the ~47 the consumer needs)
 constexpr int kLGlobRing = 2048;    // slots per inter-CTA link
 constexpr int kMaxLongCtas = 1024;
+// a spin on a link that has not advanced for this many SM cycles (≈ 2.5 s)
+// reports the link state with printf and gives up instead of hanging the GPU
+constexpr long long kWatchdogCycles = 5000000000LL;
 
 struct LongProblem {
   const void* p;
@@ -53,20 +58,32 @@ struct LongProblem {
 
 __device__ __forceinline__ uint2 ld_slot(const uint2* p) {
   uint2 v;
-  asm volatile("ld.volatile.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void st_slot(uint2* p, float v, unsigned tag) {
-  asm volatile("st.volatile.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(__float_as_uint(v)), "r"(tag)
+  asm volatile("st.relaxed.gpu.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(__float_as_uint(v)), "r"(tag)
                : "memory");
+}
+__device__ __forceinline__ void st_slot_pred(uint2* p, float v, unsigned tag, int pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %3, 0;\n\t@q st.relaxed.gpu.v2.u32 [%0], {%1, %2};\n\t}" ::"l"(p),
+      "r"(__float_as_uint(v)), "r"(tag), "r"(pred)
+      : "memory");
+}
+// two adjacent slots {v0, tag}, {v1, tag + 1} in one predicated 16-byte store
+__device__ __forceinline__ void st_slot2_pred(uint2* p, float v0, float v1, unsigned tag, int pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %5, 0;\n\t@q st.relaxed.gpu.v4.u32 [%0], {%1, %2, %3, %4};\n\t}" ::"l"(p),
+      "r"(__float_as_uint(v0)), "r"(tag), "r"(__float_as_uint(v1)), "r"(tag + 1u), "r"(pred));
 }
 __device__ __forceinline__ unsigned ld_ctr(const unsigned* p) {
   unsigned v;
-  asm volatile("ld.volatile.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void st_ctr(unsigned* p, unsigned v) {
-  asm volatile("st.volatile.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  asm volatile("st.relaxed.gpu.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // one link endpoint: ring of slots (mask = size − 1) and the consumer counter
@@ -142,35 +159,51 @@ struct LongRunner {
     for (int w = 0; w < C::EW; w++) dst[w] = reinterpret_cast<const uint4*>(f)[w];
   }
 
-  __device__ void fetch(int pos, int S, In (&a)[D], int& kind) const {
+  // positions: 0 = sentinel, p ∈ [1, m] = column p − 1, and when m + 1 is odd one
+  // more copy of the last column (repeating a point leaves δ unchanged, PAPER
+  // L259 footnote) so the stream has an even length S2 (two columns per step)
+  __device__ void fetch(int pos, int S2, In (&a)[D], int& kind) const {
 #pragma unroll
     for (int c = 0; c < D; c++) a[c] = (In)0;
-    if (pos >= S) {
+    if (pos >= S2) {
       kind = 2;
     } else if (pos == 0) {
       kind = 1;
     } else {
       kind = 0;
+      const int64_t col = min(pos - 1, m - 1);
 #pragma unroll
-      for (int c = 0; c < D; c++) a[c] = __ldg(cols + (int64_t)(pos - 1) * D + c);
+      for (int c = 0; c < D; c++) a[c] = __ldg(cols + col * D + c);
     }
   }
 
   // top value of position `pos` for this band: the corner/border for band 0,
   // else the producer's slot (spinning until its tag shows up)
-  __device__ __forceinline__ float top_of(int pos, int S, bool has_in, const Link& in, unsigned tb,
+  __device__ __forceinline__ float top_of(int pos, int S2, bool has_in, const Link& in, unsigned tb,
                                           uint2 pre) const {
-    if (pos >= S) return finf();
+    if (pos >= S2) return finf();
     if (!has_in) return pos == 0 ? 0.f : finf();
     const unsigned want = tb + (unsigned)pos + 1u;
-    while (pre.y != want) pre = ld_slot(in.ring + ((unsigned)pos & in.mask));
+    if (pre.y != want) {
+      const long long t0 = clock64();
+      while (pre.y != want) {
+        pre = ld_slot(in.ring + ((unsigned)pos & in.mask));
+        if (clock64() - t0 > kWatchdogCycles) {  // a link that never delivers: report, give up
+          printf("ffd long_kernel watchdog: consumer cta %d lane %d pos %d want tag %u saw %u (tb %u)\n",
+                 (int)blockIdx.x, lane, pos, want, pre.y, tb);
+          break;
+        }
+      }
+    }
     return __uint_as_float(pre.x);
   }
 
-  // one band of 32·R rows starting at row r0
+  // one band of 32·R rows starting at row r0, two columns per warp step
+  // (strip.cuh warp_step2: lane ℓ at step t works on columns 2(t−ℓ), 2(t−ℓ)+1)
   __device__ bool run_band(int r0, bool has_in, Link in, bool has_out, Link out, bool last_band,
                            int out_idx, int* bad_flag, unsigned tb) {
-    const int S = m + 1;
+    const int S2 = (m + 2) & ~1;  // positions (even)
+    const int NT = S2 / 2;        // steps
     bool ok = true;
     float x[NS][R], c[R];
 #pragma unroll
@@ -194,62 +227,84 @@ struct LongRunner {
     if constexpr (INT_IN) {
       if (!__all_sync(0xffffffffu, ok) && lane == 0) atomicExch(bad_flag, 1);
     }
-    float diag = finf();
+    float diag = finf(), b0 = finf();
     const uint2 none = make_uint2(0u, 0u);
-    // prologue: positions [0, 32) stored, [32, 64) prefetched
-    In a[D];
-    int kind;
-    fetch(lane, S, a, kind);
-    uint2 pre = (has_in && lane < S) ? ld_slot(in.ring + ((unsigned)lane & in.mask)) : none;
-    store_elem(a, kind, lane, top_of(lane, S, has_in, in, tb, pre), ok);
-    fetch(32 + lane, S, a, kind);
-    pre = (has_in && 32 + lane < S) ? ld_slot(in.ring + ((unsigned)(32 + lane) & in.mask)) : none;
+    // prologue: positions [0, 32) stored; column points of [32, 64) and [64, 96)
+    // in flight (two chunks ahead: one 16-step chunk does not cover the L2/HBM
+    // latency of a latency-bound warp); link slots of [32, 64) in flight
+    In a[D], a2[D];
+    int kind, kind2;
+    fetch(lane, S2, a, kind);
+    uint2 pre = (has_in && lane < S2) ? ld_slot(in.ring + ((unsigned)lane & in.mask)) : none;
+    store_elem(a, kind, lane, top_of(lane, S2, has_in, in, tb, pre), ok);
+    fetch(32 + lane, S2, a, kind);
+    fetch(64 + lane, S2, a2, kind2);
+    pre = (has_in && 32 + lane < S2) ? ld_slot(in.ring + ((unsigned)(32 + lane) & in.mask)) : none;
     __syncwarp();
-    if (has_in && lane == 0) st_ctr(in.cons, tb + (unsigned)min(32, S));
+    if (has_in && lane == 0) st_ctr(in.cons, tb + (unsigned)min(32, S2));
     unsigned cons_seen = 0, cons_next = 0;
     if (has_out) cons_seen = cons_next = ld_ctr(out.cons);
 
-    const int total = S + 31;
-    int t = 0, next_refill = 32;
+    const int total = NT + 31;
+    const int pown = (has_out && lane == kWarp - 1) ? 1 : 0;
+    const unsigned omask = out.mask & ~1u;
+    int t = 0, next_refill = 16;
     while (t < total) {
       if (t == next_refill) {
-        store_elem(a, kind, t + lane, top_of(t + lane, S, has_in, in, tb, pre), ok);
-        fetch(t + 32 + lane, S, a, kind);
-        const int pn = t + 32 + lane;
-        pre = (has_in && pn < S) ? ld_slot(in.ring + ((unsigned)pn & in.mask)) : none;
+        store_elem(a, kind, 2 * t + lane, top_of(2 * t + lane, S2, has_in, in, tb, pre), ok);
+#pragma unroll
+        for (int cc = 0; cc < D; cc++) a[cc] = a2[cc];
+        kind = kind2;
+        fetch(2 * t + 64 + lane, S2, a2, kind2);
+        const int pn = 2 * t + 32 + lane;
+        pre = (has_in && pn < S2) ? ld_slot(in.ring + ((unsigned)pn & in.mask)) : none;
         __syncwarp();
-        if (has_in && lane == 0) st_ctr(in.cons, tb + (unsigned)min(t + 32, S));
-        next_refill += 32;
+        if (has_in && lane == 0) st_ctr(in.cons, tb + (unsigned)min(2 * t + 32, S2));
+        next_refill += 16;
       }
-      if (has_out) {
-        // lane 31 writes positions ≤ t during the next 32 steps: their slots must be
-        // consumed (cons + ring > tb + t).  The counter is read one chunk ahead.
-        if (lane == kWarp - 1 && (t & 31) == 0) {
+      if (has_out && (t & 15) == 0) {
+        // lane 31 writes positions < 2t during the next 16 steps: their slots
+        // must be consumed (cons + ring > tb + 2t).  The counter is read a chunk ahead.
+        if (lane == kWarp - 1) {
           cons_seen = cons_next;
-          while ((int)(cons_seen + out.mask + 1u - (tb + (unsigned)t)) <= 0) cons_seen = ld_ctr(out.cons);
+          if ((int)(cons_seen + out.mask + 1u - (tb + 2u * (unsigned)t)) <= 0) {
+            const long long t0 = clock64();
+            while ((int)(cons_seen + out.mask + 1u - (tb + 2u * (unsigned)t)) <= 0) {
+              cons_seen = ld_ctr(out.cons);
+              if (clock64() - t0 > kWatchdogCycles) {
+                printf("ffd long_kernel watchdog: producer cta %d warp %d t %d cons %u tb %u ring %u\n",
+                       (int)blockIdx.x, (int)(threadIdx.x >> 5), t, cons_seen, tb, out.mask + 1u);
+                break;
+              }
+            }
+          }
           cons_next = ld_ctr(out.cons);
         }
       }
       __syncwarp();
       const int stop = min(next_refill, total);
       int g = t - lane;
-      if (has_out) {
+      // the ring elements of the next step are loaded one step ahead (the
+      // volatile link store would otherwise pin each load next to its use)
+      Elem2<float, KIND, D, INT_IN> ea, eb;
+      load_elem2<float, KIND, D, INT_IN>(ea, ring, g);
+      // lane 31 publishes its two bottom-row values {value, tag} of every step
+      // with one predicated 16-byte store (no divergent branch per step)
+      auto one = [&](const Elem2<float, KIND, D, INT_IN>& el, int gg) {
+        step2_compute<float, KIND, D, R, INT_IN>(c, diag, b0, x, el, lane);
+        st_slot2_pred(out.ring + ((2u * (unsigned)gg) & omask), b0, c[R - 1],
+                      tb + 2u * (unsigned)gg + 1u, pown & ((unsigned)gg < (unsigned)NT));
+      };
 #pragma unroll 1
-        for (; t < stop; ++t, ++g) {
-          warp_step<float, KIND, D, R, INT_IN>(c, diag, x, ring, g, lane);
-          if (lane == kWarp - 1 && g >= 0 && g < S)
-            st_slot(out.ring + ((unsigned)g & out.mask), c[R - 1], tb + (unsigned)g + 1u);
-        }
-      } else {
-#pragma unroll 1
-        for (; t + 2 <= stop; t += 2, g += 2) {
-          warp_step<float, KIND, D, R, INT_IN>(c, diag, x, ring, g, lane);
-          warp_step<float, KIND, D, R, INT_IN>(c, diag, x, ring, g + 1, lane);
-        }
-        if (t < stop) {
-          warp_step<float, KIND, D, R, INT_IN>(c, diag, x, ring, g, lane);
-          ++t;
-        }
+      for (; t + 2 <= stop; t += 2, g += 2) {
+        load_elem2<float, KIND, D, INT_IN>(eb, ring, g + 1);
+        one(ea, g);
+        load_elem2<float, KIND, D, INT_IN>(ea, ring, g + 2);
+        one(eb, g + 1);
+      }
+      if (t < stop) {
+        one(ea, g);
+        ++t;
       }
     }
     const bool all_ok = __all_sync(0xffffffffu, ok);
@@ -285,9 +340,13 @@ template <int KIND, int D, bool INT_IN, int FIN>
 __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProblem pb) {
   using C = SCfg<float, KIND, D, INT_IN>;
   using In = typename std::conditional<INT_IN, int32_t, float>::type;
-  __shared__ uint4 rings[kLWarps][kRing * C::EW];
-  __shared__ uint2 slink[kLWarps][kLSmemRing];
-  __shared__ unsigned scons[kLWarps];
+  // dynamic shared memory: [kLWarps][kLSmemRing] link slots, [kLWarps][kRing·EW]
+  // column rings, [kLWarps] consumer counters
+  extern __shared__ uint4 lsm[];
+  uint2 (*slink)[kLSmemRing] = reinterpret_cast<uint2(*)[kLSmemRing]>(lsm);
+  uint4 (*rings)[kRing * C::EW] =
+      reinterpret_cast<uint4(*)[kRing * C::EW]>(lsm + kLWarps * kLSmemRing / 2);
+  unsigned* scons = reinterpret_cast<unsigned*>(lsm + kLWarps * kLSmemRing / 2 + kLWarps * kRing * C::EW);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x, cta = blockIdx.x;
   for (int i = threadIdx.x; i < kLWarps * kLSmemRing; i += blockDim.x)
@@ -307,7 +366,7 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
     const In* cols = reinterpret_cast<const In*>(swap ? pb.p : pb.q) +
                      (swap ? pb.offsets[k] : pb.offsets[B + k]) * D;
     const int R = long_rows_per_lane(n, G);
-    const int S = m + 1;
+    const int S = (m + 2) & ~1;  // stream positions of this pair (even, see run_band)
     if (R == 0) {
       if (cta == 0 && threadIdx.x == 0) {
         if constexpr (INT_IN) reinterpret_cast<long long*>(pb.out)[k] = LLONG_MIN;
@@ -380,14 +439,18 @@ struct LongWs {
 template <int KIND, int D, bool INT_IN, int FIN>
 cudaError_t launch_long_k(const LongArgs& a, int sms, cudaStream_t st, const LongWs& w, int G) {
   auto k = long_kernel<KIND, D, INT_IN, FIN>;
+  using C = SCfg<float, KIND, D, INT_IN>;
+  const size_t smem = sizeof(uint2) * kLWarps * kLSmemRing + sizeof(uint4) * kLWarps * kRing * C::EW +
+                      sizeof(unsigned) * kLWarps;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kWarp * kLWarps, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kWarp * kLWarps, smem);
   if (occ < 1) return cudaErrorLaunchOutOfResources;
   if (G > sms * occ) G = sms * occ;
   LongProblem pb{a.p,      a.q,       a.offsets, a.lengths, a.num_pairs, a.list,
                  a.list_count, a.out, w.gring,   w.gcons,   w.bad};
   void* args[] = {&pb};
-  return cudaLaunchCooperativeKernel((const void*)k, dim3(G), dim3(kWarp * kLWarps), args, 0, st);
+  return cudaLaunchCooperativeKernel((const void*)k, dim3(G), dim3(kWarp * kLWarps), args, smem, st);
 }
 
 // per-dimension dispatch (longpair_d<D>.cu)

@@ -79,7 +79,7 @@ __global__ void op_kernel(float* out, long long* cyc, int iters) {
 // 7: FMNMX3+IADD3.  instr_per_unit is the number of instructions per chain unit.
 template <int MIX>
 __global__ void mix_kernel(float* out, long long* cyc, int iters) {
-  float a[NCHAIN], b[NCHAIN];
+  float a[NCHAIN], b[NCHAIN], x_acc[NCHAIN], y_acc[NCHAIN];
   int ia[NCHAIN];
   uint64_t p[NCHAIN], q[NCHAIN];
   float y = 1.0001f + threadIdx.x * 1e-7f, z = 0.9999f - threadIdx.x * 1e-7f;
@@ -89,6 +89,8 @@ __global__ void mix_kernel(float* out, long long* cyc, int iters) {
   for (int u = 0; u < NCHAIN; u++) {
     a[u] = threadIdx.x * 0.001f + u;
     b[u] = threadIdx.x * 0.002f - u;
+    x_acc[u] = 0.f;
+    y_acc[u] = 0.f;
     ia[u] = threadIdx.x * 3 + u;
     p[u] = pack(a[u], a[u] + 1.f);
     q[u] = pack(b[u], b[u] + 2.f);
@@ -121,6 +123,46 @@ __global__ void mix_kernel(float* out, long long* cyc, int iters) {
           asm volatile("max.f32 %0, %0, %1;" : "+f"(b[u]) : "f"(y));
         if (MIX == 4) asm volatile("max.f32 %0, %0, %1;" : "+f"(a[u]) : "f"(z));
         if (MIX == 6 || MIX == 7) asm volatile("add.s32 %0, %0, %1;" : "+r"(ia[u]) : "r"(yi));
+        if (MIX == 8) {  // fp32 3-D SQ, two cells: 3 FADD2, FMUL2, 2 FFMA2, 2 FMNMX3, 2 FMNMX
+          asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(p[u]) : "l"(y2));
+          asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(q[u]) : "l"(y2));
+          asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(p[u]) : "l"(z2));
+          asm volatile("mul.rn.f32x2 %0, %0, %1;" : "+l"(q[u]) : "l"(z2));
+          asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(p[u]) : "l"(y2), "l"(z2));
+          asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(q[u]) : "l"(z2), "l"(y2));
+        }
+        if (MIX == 8) {  // 2 x (FMNMX3 + FMNMX) on two chains
+          float t;
+          asm volatile("min.f32 %0, %1, %2;\n\tmin.f32 %0, %0, %3;" : "=f"(t) : "f"(a[u]), "f"(y), "f"(z));
+          a[u] = t;
+          asm volatile("min.f32 %0, %1, %2;\n\tmin.f32 %0, %0, %3;" : "=f"(t) : "f"(b[u]), "f"(z), "f"(y));
+          b[u] = t;
+          asm volatile("max.f32 %0, %0, %1;" : "+f"(a[u]) : "f"(z));
+          asm volatile("max.f32 %0, %0, %1;" : "+f"(b[u]) : "f"(y));
+        }
+        if (MIX == 9 || MIX == 10) {  // fp32 2-D L1 / Linf, two cells: 2 FADD2 + 2 (|a| op |b|)
+          // + 2 x (FMNMX3 + FMNMX); the distance feeds the max, as in the DP cell
+          asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(p[u]) : "l"(y2));
+          asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(q[u]) : "l"(z2));
+          float r1, r2, t;
+          if (MIX == 9) {
+            asm volatile("{.reg .f32 l, h, al, ah; mov.b64 {l, h}, %1; abs.f32 al, l; abs.f32 ah, h; add.rn.f32 %0, al, ah;}"
+                         : "=f"(r1) : "l"(p[u]));
+            asm volatile("{.reg .f32 l, h, al, ah; mov.b64 {l, h}, %1; abs.f32 al, l; abs.f32 ah, h; add.rn.f32 %0, al, ah;}"
+                         : "=f"(r2) : "l"(q[u]));
+          } else {
+            asm volatile("{.reg .f32 l, h, al, ah; mov.b64 {l, h}, %1; abs.f32 al, l; abs.f32 ah, h; max.f32 %0, al, ah;}"
+                         : "=f"(r1) : "l"(p[u]));
+            asm volatile("{.reg .f32 l, h, al, ah; mov.b64 {l, h}, %1; abs.f32 al, l; abs.f32 ah, h; max.f32 %0, al, ah;}"
+                         : "=f"(r2) : "l"(q[u]));
+          }
+          asm volatile("min.f32 %0, %1, %2;\n\tmin.f32 %0, %0, %3;" : "=f"(t) : "f"(a[u]), "f"(y), "f"(z));
+          a[u] = t;
+          asm volatile("min.f32 %0, %1, %2;\n\tmin.f32 %0, %0, %3;" : "=f"(t) : "f"(b[u]), "f"(z), "f"(y));
+          b[u] = t;
+          asm volatile("max.f32 %0, %0, %1;" : "+f"(a[u]) : "f"(r1));
+          asm volatile("max.f32 %0, %0, %1;" : "+f"(b[u]) : "f"(r2));
+        }
       }
     }
   }
@@ -128,7 +170,7 @@ __global__ void mix_kernel(float* out, long long* cyc, int iters) {
   float s = 0.f;
 #pragma unroll
   for (int u = 0; u < NCHAIN; u++)
-    s += a[u] + b[u] + (float)ia[u] + __uint_as_float((uint32_t)p[u]) + __uint_as_float((uint32_t)q[u]);
+    s += a[u] + b[u] + x_acc[u] + y_acc[u] + (float)ia[u] + __uint_as_float((uint32_t)p[u]) + __uint_as_float((uint32_t)q[u]);
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
@@ -294,6 +336,14 @@ int main() {
   run("mix_FMNMX3+FMNMX", mix_kernel<5>, 4, 256, IT, per * 2, "warp-instr");
   run("mix_FFMA2+IADD3", mix_kernel<6>, 4, 256, IT, per * 2, "warp-instr");
   run("mix_FMNMX3+IADD3", mix_kernel<7>, 4, 256, IT, per * 2, "warp-instr");
+  // the same mixes reported as cells per clock per SM (32 lanes x cells per unit)
+  run("mixcells_f32_d2_sq", mix_kernel<3>, 4, 256, IT, per * 32, "cells");
+  run("mixcells_xsq_d2", mix_kernel<4>, 4, 256, IT, per * 64, "cells");
+  run("mixcells_f32_d3_sq", mix_kernel<8>, 4, 256, IT, per * 64, "cells");
+  run("mixcells_f32_d2_l1", mix_kernel<9>, 4, 256, IT, per * 64, "cells");
+  run("mixcells_f32_d2_linf", mix_kernel<10>, 4, 256, IT, per * 64, "cells");
+  run("mixcells_xsq_d2_w16", mix_kernel<4>, 2, 256, IT, per * 64, "cells");
+  run("mixcells_f32_d2_sq_w16", mix_kernel<3>, 2, 256, IT, per * 32, "cells");
   // cells per clock per SM: per thread-step = R cells; lanes x warps
   const int ST = 4000;
   int wl[3] = {8, 16, 32};

@@ -44,6 +44,10 @@ ISSUE_PER_CELL = {"f32_d2_sq": 4.0, "xsq_d2": 3.5, "f32_d3_sq": 5.0, "f32_d2_l1"
 CELL_OF_CONFIG = {1: "f32_d2_sq", 2: "xsq_d2", 3: "f32_d3_sq", 4: "f32_d2_sq", 5: "f32_d2_sq"}
 CELL_OF_NORM = {"l1": "f32_d2_l1", "l2": "f32_d2_sq", "linf": "f32_d2_linf"}
 MIX_SOURCE = "profiles/r1_microbench_pipes_v2.jsonl (tools/microbench/pipes.cu mixcells_*)"
+# dram__bytes_read.sum + dram__bytes_write.sum of one launch of the dominant kernel, from the
+# committed `ncu --set full` capture (profiles/r1_c2_batch_ncu_full_v3.txt: 536.6 MB + 9.4 MB);
+# --traffic overrides.  Algorithmic bytes per launch for c2: 514.3 MB in + 0.8 MB out.
+TRAFFIC_BYTES = {2: 546.0e6}
 
 
 def alu_roofline(cells_per_launch, kernel_ms, cell, sms, f_max, f_meas, kernel, traffic):
@@ -330,8 +334,10 @@ def bench_ffd(args):
     f_max = (clocks["sm_max_mhz"] or SM_MAX_MHZ_NOMINAL) * 1e6
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     cell = CELL_OF_CONFIG[cfg.cid]
+    traffic = args.traffic if args.traffic is not None else TRAFFIC_BYTES.get(cfg.cid)
     roofline = alu_roofline(cells, kern_ms, cell, sms, f_max, f_meas,
-                            f"batch_kernel ({cell} cell)", args.traffic)
+                            f"batch_kernel ({cell} cell)", traffic)
+    roofline["algorithmic_bytes"] = b.p.nbytes + b.q.nbytes + b.offsets.nbytes + b.lengths.nbytes + out.numel() * out.element_size()
 
     cpu = cpu_baseline_line(args, cfg, ws)
 

@@ -41,8 +41,10 @@ struct CdistProblem {
   int64_t tiles_b;
 };
 
+constexpr int kCdMinCtasPerSm = 4;  // 128 registers/thread: the W=8, R=16 shape needs ~100
+
 template <int KIND, int D, int W, int R, int FIN>
-__global__ void __launch_bounds__(kWarp* kWarpsPerCta, kMinCtasPerSm)
+__global__ void __launch_bounds__(kWarp* kWarpsPerCta, kCdMinCtasPerSm)
     cdist_kernel(const CdistProblem pb) {
   using C = SCfg<float, KIND, D, false>;
   static_assert(!C::XSQ, "cdist: fp32 inputs");

@@ -29,7 +29,7 @@ __global__ void prep_keys_kernel(const int64_t* __restrict__ offsets,
       const bool swap = n > m;
       const int rows = swap ? m : n, cols = swap ? n : m;
       const int nb = (rows + kWarp * kMaxR - 1) / (kWarp * kMaxR);
-      if (nb > kMaxBands || (nb > 1 && 2 * ((cols + 2) / 2) + 2 > kScratchCols)) {
+      if (nb > kMaxBands || (nb > 1 && cols + 2 > kScratchCols)) {
         long_list[atomicAdd(long_count, 1)] = (int)k;
       } else {
         const int R = (rows + kWarp * nb - 1) / (kWarp * nb);

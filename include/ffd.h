@@ -79,6 +79,19 @@ int ffd_batch(const void* p, const void* q, const int64_t* offsets, const int32_
               void* workspace, size_t workspace_bytes, ffd_stream_t stream);
 size_t ffd_batch_workspace_bytes(int64_t num_pairs);
 
+/* ffd_batch_dtw — dynamic time warping of B pairs (PAPER Appendix B:
+ *   Alg. 2 with max replaced by +, i.e. C[i][j] = min{C[i−1][j], C[i−1][j−1],
+ *   C[i][j−1]} + d_ij, result C[P][Q]).  Same arguments, layout, workspace and
+ *   stream semantics as ffd_batch.  dtype must be FFD_F32 (FFD_ERR_UNSUPPORTED
+ *   otherwise); FFD_L2 evaluates sqrt per cell; sums are accumulated in fp32 in
+ *   the DP's own order (relative error ≤ (n+m+D+2)·2⁻²⁴ of the exact value).
+ *   Pairs whose shorter curve needs more than 8 bands of 512 rows, or more than
+ *   one band with the longer curve above 2046 points, get NaN (no long-pair path
+ *   for DTW).                                                                    */
+int ffd_batch_dtw(const void* p, const void* q, const int64_t* offsets, const int32_t* lengths,
+                  int64_t num_pairs, int32_t dim, int32_t norm, int32_t dtype, void* out,
+                  void* workspace, size_t workspace_bytes, ffd_stream_t stream);
+
 /* ffd_batch_host — the same computation from HOST buffers (end-to-end path).
  *   p_host: [np, dim], q_host: [nq, dim]; offsets_host/lengths_host as above;
  *   out_host: float[B] / int64[B].  Host buffers should be pinned for overlap.

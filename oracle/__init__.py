@@ -64,7 +64,7 @@ def _declare(L):
         getattr(L, n).argtypes = [_P, _I64, _P, _I64, _INT, _INT, _P]
     for n in ("orc_frechet_table_d", "orc_frechet_linear_d", "orc_frechet_alg2_d",
               "orc_frechet_inplace_d", "orc_frechet_brute_d", "orc_hausdorff_d",
-              "orc_dtw_table_d", "orc_dtw_alg_d"):
+              "orc_dtw_table_d", "orc_dtw_alg_d", "orc_dtw_brute_d"):
         getattr(L, n).restype = ctypes.c_double
         getattr(L, n).argtypes = [_P, _I64, _I64]
     for n in ("orc_frechet_table_i", "orc_frechet_linear_i", "orc_frechet_brute_i"):
@@ -73,10 +73,11 @@ def _declare(L):
     L.orc_frechet_full_table_d.restype = None
     L.orc_frechet_full_table_d.argtypes = [_P, _I64, _I64, _P]
     for n in ("orc_pair_f32", "orc_pair_linear_f32", "orc_pair_i32", "orc_pair_linear_i32",
-              "orc_pair_f32mirror"):
+              "orc_pair_f32mirror", "orc_pair_dtw_f32", "orc_pair_dtw_f32mirror"):
         getattr(L, n).restype = _INT
         getattr(L, n).argtypes = [_P, _I64, _P, _I64, _INT, _INT, _P]
-    for n in ("orc_batch_f32", "orc_batch_f32mirror", "orc_batch_i32"):
+    for n in ("orc_batch_f32", "orc_batch_f32mirror", "orc_batch_i32", "orc_batch_dtw_f32",
+              "orc_batch_dtw_f32mirror"):
         getattr(L, n).restype = _INT
         getattr(L, n).argtypes = [_P, _P, _P, _P, _I64, _INT, _INT, _P, _INT]
     for n in ("orc_cdist_entries_f32", "orc_cdist_entries_f32mirror"):
@@ -174,6 +175,36 @@ def dtw_table_d(d):
 
 def dtw_alg_d(d):
     return _from_d(lib().orc_dtw_alg_d, None, d)
+
+
+def dtw_brute_d(d):
+    return _from_d(lib().orc_dtw_brute_d, None, d)
+
+
+def dtw_pair(p, q, norm="l2", mirror=False):
+    """DTW(p, q) of float32 curves with lazily evaluated d: fp64 table, or the
+    fp32 mirror of the kernels' operation order (mirror=True)."""
+    p, q = _c(p, np.float32), _c(q, np.float32)
+    out = np.zeros(1, np.float32 if mirror else np.float64)
+    fn = lib().orc_pair_dtw_f32mirror if mirror else lib().orc_pair_dtw_f32
+    st = fn(_ptr(p), p.shape[0], _ptr(q), q.shape[0], p.shape[1], _norm(norm), _ptr(out))
+    if st:
+        raise OracleError(st)
+    return out[0].item()
+
+
+def dtw_batch(p, q, offsets, lengths, dim, norm="l2", threads=0, mirror=False, check=True):
+    """DTW of every pair of a batch (float32 curves), layout as batch()."""
+    offsets = _c(offsets, np.int64)
+    lengths = _c(lengths, np.int32)
+    B = offsets.shape[0] // 2
+    p, q = _c(p, np.float32), _c(q, np.float32)
+    out = np.empty(B, np.float32 if mirror else np.float64)
+    fn = lib().orc_batch_dtw_f32mirror if mirror else lib().orc_batch_dtw_f32
+    st = fn(_ptr(p), _ptr(q), _ptr(offsets), _ptr(lengths), B, dim, _norm(norm), _ptr(out), threads)
+    if st and check:
+        raise OracleError(st)
+    return out
 
 
 # ---- pairs -----------------------------------------------------------------

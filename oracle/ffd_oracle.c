@@ -619,3 +619,118 @@ double orc_dtw_alg_d(const double* d, int64_t P, int64_t Q) {
   free(t); free(a);
   return r;
 }
+
+/* ------------------------------------------------------------------------- */
+/* DTW by definition, for pinning: min over all monotone couplings (the same  */
+/* couplings as the Fréchet brute force) of the SUM of d along */
+/* the coupling.  Exponential: P, Q ≤ 10 only.                                */
+/* ------------------------------------------------------------------------- */
+static double dtw_brute_rec(const double* d, int64_t P, int64_t Q, int64_t i, int64_t j, double acc) {
+  acc += d[i * Q + j];
+  if (i == P - 1 && j == Q - 1) return acc;
+  double best = INFINITY;
+  if (i + 1 < P) best = dmin2(best, dtw_brute_rec(d, P, Q, i + 1, j, acc));
+  if (j + 1 < Q) best = dmin2(best, dtw_brute_rec(d, P, Q, i, j + 1, acc));
+  if (i + 1 < P && j + 1 < Q) best = dmin2(best, dtw_brute_rec(d, P, Q, i + 1, j + 1, acc));
+  return best;
+}
+
+double orc_dtw_brute_d(const double* d, int64_t P, int64_t Q) {
+  if (P < 1 || Q < 1 || P > 10 || Q > 10) return NAN;
+  return dtw_brute_rec(d, P, Q, 0, 0, 0.0);
+}
+
+/* DTW of one pair with lazily evaluated d (fp64; table rows of Appendix B's   */
+/* recurrence): C[0][0]=0, borders +inf,                      */
+/* C[i][j] = d(p_{i-1}, q_{j-1}) + min(C[i-1][j], C[i-1][j-1], C[i][j-1]).     */
+int orc_pair_dtw_f32(const float* p, int64_t P, const float* q, int64_t Q, int dim, int norm,
+                     double* out) {
+  int st = check_norm_f(dim, norm);
+  if (st) return st;
+  if (P < 1 || Q < 1) return ORC_ERR_EMPTY;
+  if (check_finite(p, P, dim) || check_finite(q, Q, dim)) return ORC_ERR_NONFINITE;
+  double* prev = (double*)malloc(sizeof(double) * (size_t)(Q + 1));
+  double* cur = (double*)malloc(sizeof(double) * (size_t)(Q + 1));
+  if (!prev || !cur) { free(prev); free(cur); return ORC_ERR_ARG; }
+  prev[0] = 0.0;
+  for (int64_t j = 1; j <= Q; j++) prev[j] = INFINITY;
+  for (int64_t i = 1; i <= P; i++) {
+    cur[0] = INFINITY;
+    for (int64_t j = 1; j <= Q; j++)
+      cur[j] = orc_point_dist_f32(p + (i - 1) * dim, q + (j - 1) * dim, dim, norm) +
+               dmin3(prev[j], prev[j - 1], cur[j - 1]);
+    double* t = prev; prev = cur; cur = t;
+  }
+  *out = prev[Q];
+  free(prev); free(cur);
+  return ORC_OK;
+}
+
+/* DTW fp32 mirror: the same table in fp32 with the kernels' operation order: */
+/* d as in mirror_dist (L2: sqrtf of the squared sum, per cell — a sum of     */
+/* distances cannot take the root once at the end), c = min(min(up, diag),    */
+/* left) + d with one fp32 rounding per cell.                                  */
+int orc_pair_dtw_f32mirror(const float* p, int64_t P, const float* q, int64_t Q, int dim, int norm,
+                           float* out) {
+  int st = check_norm_f(dim, norm);
+  if (st) return st;
+  if (P < 1 || Q < 1) return ORC_ERR_EMPTY;
+  if (check_finite(p, P, dim) || check_finite(q, Q, dim)) return ORC_ERR_NONFINITE;
+  float* prev = (float*)malloc(sizeof(float) * (size_t)(Q + 1));
+  float* cur = (float*)malloc(sizeof(float) * (size_t)(Q + 1));
+  if (!prev || !cur) { free(prev); free(cur); return ORC_ERR_ARG; }
+  prev[0] = 0.0f;
+  for (int64_t j = 1; j <= Q; j++) prev[j] = INFINITY;
+  for (int64_t i = 1; i <= P; i++) {
+    cur[0] = INFINITY;
+    for (int64_t j = 1; j <= Q; j++) {
+      float dij = mirror_dist(p + (i - 1) * dim, q + (j - 1) * dim, dim, norm);
+      if (norm == ORC_L2) dij = sqrtf(dij);
+      cur[j] = fminf(fminf(prev[j], prev[j - 1]), cur[j - 1]) + dij;
+    }
+    float* t = prev; prev = cur; cur = t;
+  }
+  *out = prev[Q];
+  free(prev); free(cur);
+  return ORC_OK;
+}
+
+int orc_batch_dtw_f32(const float* p, const float* q, const int64_t* offsets,
+                      const int32_t* lengths, int64_t B, int dim, int norm, double* out,
+                      int threads) {
+  int first = ORC_OK;
+  int nt = threads_or_default(threads);
+  (void)nt;
+#pragma omp parallel for schedule(dynamic, 8) num_threads(nt)
+  for (int64_t k = 0; k < B; k++) {
+    double r = NAN;
+    int st = orc_pair_dtw_f32(p + offsets[k] * dim, lengths[k], q + offsets[B + k] * dim,
+                              lengths[B + k], dim, norm, &r);
+    out[k] = st ? NAN : r;
+    if (st) {
+#pragma omp critical
+      if (first == ORC_OK) first = st;
+    }
+  }
+  return first;
+}
+
+int orc_batch_dtw_f32mirror(const float* p, const float* q, const int64_t* offsets,
+                            const int32_t* lengths, int64_t B, int dim, int norm, float* out,
+                            int threads) {
+  int first = ORC_OK;
+  int nt = threads_or_default(threads);
+  (void)nt;
+#pragma omp parallel for schedule(dynamic, 8) num_threads(nt)
+  for (int64_t k = 0; k < B; k++) {
+    float r = NAN;
+    int st = orc_pair_dtw_f32mirror(p + offsets[k] * dim, lengths[k], q + offsets[B + k] * dim,
+                                    lengths[B + k], dim, norm, &r);
+    out[k] = st ? NAN : r;
+    if (st) {
+#pragma omp critical
+      if (first == ORC_OK) first = st;
+    }
+  }
+  return first;
+}

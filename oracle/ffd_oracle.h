@@ -111,6 +111,20 @@ int orc_cdist_entries_f32mirror(const float* A, int32_t lenA, const float* B, in
 /* ---- DTW (PAPER Appendix B): max replaced by + ------------------ */
 double orc_dtw_table_d(const double* d, int64_t P, int64_t Q);
 double orc_dtw_alg_d(const double* d, int64_t P, int64_t Q);
+/* DTW by definition (min over monotone couplings of the sum of d), P,Q ≤ 10 */
+double orc_dtw_brute_d(const double* d, int64_t P, int64_t Q);
+/* DTW of curve pairs: fp64 table with lazily evaluated d, and the fp32 mirror
+ * of the kernels' operation order (L2: sqrt per cell) — DESIGN.md §DTW       */
+int orc_pair_dtw_f32(const float* p, int64_t P, const float* q, int64_t Q, int dim, int norm,
+                     double* out);
+int orc_pair_dtw_f32mirror(const float* p, int64_t P, const float* q, int64_t Q, int dim, int norm,
+                           float* out);
+int orc_batch_dtw_f32(const float* p, const float* q, const int64_t* offsets,
+                      const int32_t* lengths, int64_t B, int dim, int norm, double* out,
+                      int threads);
+int orc_batch_dtw_f32mirror(const float* p, const float* q, const int64_t* offsets,
+                            const int32_t* lengths, int64_t B, int dim, int norm, float* out,
+                            int threads);
 
 #ifdef __cplusplus
 }

@@ -7,6 +7,7 @@ memory and streams.  There is no CPU fallback: if the library or a GPU is
 missing, calls raise.
 
     batch(p, q, offsets, lengths, norm)        -> Tensor[B]   (ffd_batch)
+    dtw_batch(p, q, offsets, lengths, norm)    -> Tensor[B]   (ffd_batch_dtw)
     batch_host(p, q, offsets, lengths, norm)   -> ndarray[B]  (ffd_batch_host)
     cdist(A, B, norm, rows=None)               -> Tensor      (ffd_cdist)
     validate(p, q, offsets, lengths)           -> status      (ffd_validate_batch)
@@ -49,6 +50,8 @@ def lib():
         P, I64, I32_, SZ = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_size_t
         L.ffd_batch.argtypes = [P, P, P, P, I64, I32_, I32_, I32_, P, P, SZ, P]
         L.ffd_batch.restype = ctypes.c_int
+        L.ffd_batch_dtw.argtypes = [P, P, P, P, I64, I32_, I32_, I32_, P, P, SZ, P]
+        L.ffd_batch_dtw.restype = ctypes.c_int
         L.ffd_batch_workspace_bytes.argtypes = [I64]
         L.ffd_batch_workspace_bytes.restype = SZ
         L.ffd_batch_host.argtypes = [P, I64, P, I64, P, P, I64, I32_, I32_, I32_, P, P]
@@ -72,7 +75,7 @@ def lib():
     return _lib
 
 
-EXPORTED = ["ffd_batch", "ffd_batch_workspace_bytes", "ffd_batch_host", "ffd_cdist",
+EXPORTED = ["ffd_batch", "ffd_batch_dtw", "ffd_batch_workspace_bytes", "ffd_batch_host", "ffd_cdist",
             "ffd_cdist_workspace_bytes", "ffd_validate_batch", "ffd_status_string",
             "ffd_take_launch_count", "ffd_version", "ffd_profile_enable", "ffd_profile_take"]
 
@@ -137,10 +140,11 @@ def launches_taken() -> int:
     return int(lib().ffd_take_launch_count())
 
 
-def batch(p, q, offsets, lengths, norm="l2", out=None, stream=None):
+def batch(p, q, offsets, lengths, norm="l2", out=None, stream=None, measure="frechet"):
     """δ_dF for B pairs (ffd_batch).  p [Σn, dim], q [Σm, dim] float32/int32 CUDA
     tensors; offsets int64[2B]; lengths int32[2B].  Returns float32[B] (fp32
-    input) or int64[B] (int32 input)."""
+    input) or int64[B] (int32 input).  measure="dtw": dynamic time warping
+    (ffd_batch_dtw, PAPER Appendix B; float32 input only)."""
     torch = _torch()
     if not (p.is_cuda and q.is_cuda and offsets.is_cuda and lengths.is_cuda):
         raise ValueError("batch() takes CUDA tensors; use batch_host() for host arrays")
@@ -154,10 +158,18 @@ def batch(p, q, offsets, lengths, norm="l2", out=None, stream=None):
         out = torch.empty(B, dtype=torch.int64 if dt == I32 else torch.float32, device=p.device)
     ws_bytes = lib().ffd_batch_workspace_bytes(B)
     ws = workspace(ws_bytes, p.device)
-    _check(lib().ffd_batch(p.data_ptr(), q.data_ptr(), offsets.data_ptr(), lengths.data_ptr(), B, dim,
-                           _norm(norm), dt, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)),
-           "ffd_batch")
+    if measure not in ("frechet", "dtw"):
+        raise ValueError(f"unknown measure {measure!r}")
+    fn = lib().ffd_batch if measure == "frechet" else lib().ffd_batch_dtw
+    _check(fn(p.data_ptr(), q.data_ptr(), offsets.data_ptr(), lengths.data_ptr(), B, dim,
+              _norm(norm), dt, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)),
+           "ffd_batch" if measure == "frechet" else "ffd_batch_dtw")
     return out
+
+
+def dtw_batch(p, q, offsets, lengths, norm="l2", out=None, stream=None):
+    """Dynamic time warping of B pairs (ffd_batch_dtw): same layout as batch()."""
+    return batch(p, q, offsets, lengths, norm=norm, out=out, stream=stream, measure="dtw")
 
 
 def batch_host(p: np.ndarray, q: np.ndarray, offsets: np.ndarray, lengths: np.ndarray, norm="l2",

@@ -127,11 +127,13 @@ static int check_common(int32_t dim, int32_t norm, int32_t dtype) {
   return FFD_OK;
 }
 
+// measure: 0 discrete Fréchet (Eq. (1)), 1 DTW (Appendix B)
 static int batch_impl(const void* p, const void* q, const int64_t* offsets, const int32_t* lengths,
                       int64_t B, int32_t dim, int32_t norm, int32_t dtype, void* out,
-                      void* workspace, size_t ws_bytes, cudaStream_t st) {
+                      void* workspace, size_t ws_bytes, cudaStream_t st, int measure = 0) {
   int s = check_common(dim, norm, dtype);
   if (s) return s;
+  if (measure == 1 && dtype != FFD_F32) return FFD_ERR_UNSUPPORTED;
   if (B < 0) return FFD_ERR_ARG;
   if (B == 0) return FFD_OK;
   if (!p || !q || !offsets || !lengths || !out) return FFD_ERR_ARG;
@@ -141,8 +143,12 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
   if (!workspace || ws_bytes < ws.bytes) return FFD_ERR_WORKSPACE;
 
   const int int_in = dtype == FFD_I32;
-  const int kind = kind_for(norm, dtype);
-  const int fin = (norm == FFD_L2) ? F_SQRT : F_NONE;
+  int kind = kind_for(norm, dtype);
+  int fin = (norm == FFD_L2) ? F_SQRT : F_NONE;
+  if (measure == 1) {  // DTW: L2 needs the per-cell square root (sums do not commute with it)
+    if (norm == FFD_L2) kind = K_SQRT;
+    fin = F_DTW;
+  }
   const BatchEntry* main_e = find_batch(BatchKey{0, kind, dim, int_in, fin});
   if (!main_e) return FFD_ERR_UNSUPPORTED;
   const BatchEntry* fb_e = nullptr;
@@ -157,7 +163,8 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
                       reinterpret_cast<char*>(ws.cursor) - reinterpret_cast<char*>(ws.counters),
                       st) != cudaSuccess)
     return FFD_ERR_CUDA;
-  if (launch_prep(offsets, lengths, B, int_in, out, ws, di.sms, st, &g_launches) != cudaSuccess)
+  if (launch_prep(offsets, lengths, B, int_in, measure == 0, out, ws, di.sms, st, &g_launches) !=
+      cudaSuccess)
     return FFD_ERR_CUDA;
 
   Problem pb{};
@@ -197,6 +204,7 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
     ++g_launches;
   }
 
+  if (measure != 0) return FFD_OK;  // DTW: no long-pair path (prep wrote NaN for those pairs)
   // pairs too long for the band scratch of the batch kernel: cross-CTA wavefront
   LongArgs la{};
   la.p = p;
@@ -285,6 +293,13 @@ int ffd_batch(const void* p, const void* q, const int64_t* offsets, const int32_
               void* workspace, size_t workspace_bytes, ffd_stream_t stream) {
   return batch_impl(p, q, offsets, lengths, num_pairs, dim, norm, dtype, out, workspace,
                     workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ffd_batch_dtw(const void* p, const void* q, const int64_t* offsets, const int32_t* lengths,
+                  int64_t num_pairs, int32_t dim, int32_t norm, int32_t dtype, void* out,
+                  void* workspace, size_t workspace_bytes, ffd_stream_t stream) {
+  return batch_impl(p, q, offsets, lengths, num_pairs, dim, norm, dtype, out, workspace,
+                    workspace_bytes, reinterpret_cast<cudaStream_t>(stream), 1);
 }
 
 int ffd_batch_host(const void* p_host, int64_t np, const void* q_host, int64_t nq,

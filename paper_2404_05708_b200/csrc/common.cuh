@@ -13,10 +13,15 @@ enum Kind : int {
   K_L1 = 1,    // Σ |Δ|
   K_LINF = 2,  // max |Δ|
   K_XSQ = 3,   // int32 input, Σ Δ² as |p'|² + |q'|² − 2 p'·q' in fp32-exact integer arithmetic
+  K_SQRT = 4,  // sqrt(Σ Δ²) per cell (DTW under L2: a sum of distances cannot hoist the sqrt)
 };
 
 // output finalisation
-enum Fin : int { F_NONE = 0, F_SQRT = 1 };
+// output finalisation / measure: F_DTW selects the dynamic-time-warping cell
+// c = min3(up, diag, left) + d (PAPER Appendix B) instead of Fréchet's
+// max(min3, d); its result is read from the lane holding row n−1 (no row padding
+// is neutral for a sum).
+enum Fin : int { F_NONE = 0, F_SQRT = 1, F_DTW = 2 };
 
 constexpr int kWarp = 32;
 constexpr int kRing = 128;          // column-stream ring entries per warp (power of two)

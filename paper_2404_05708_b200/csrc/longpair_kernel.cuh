@@ -21,6 +21,12 @@
 //     column ring, and re-polls only the slots that were not ready.  It
 //     publishes how far it has consumed; the producer checks that counter (also
 //     prefetched) before reusing slots: bounded rings, no overwrite.
+//   * Slots are indexed by the ABSOLUTE stream position (tag base + position) so
+//     that slot reuse distance is exactly the ring size across successive pairs —
+//     the flow-control test (consumed + ring > absolute position) is only valid
+//     then.  (Indexing by the position within a pair let a producer that had
+//     moved on to the next pair overwrite the previous pair's last unconsumed
+//     slots whenever a stream length was not a multiple of the ring size: a hang.)
 //   * One persistent CTA of 8 warps per SM, cooperative launch: all bands are
 //     co-resident, so spinning on a neighbour cannot deadlock.  Counters and
 //     tags are absolute positions, so successive long pairs need no grid barrier.
@@ -187,7 +193,7 @@ struct LongRunner {
     if (pre.y != want) {
       const long long t0 = clock64();
       while (pre.y != want) {
-        pre = ld_slot(in.ring + ((unsigned)pos & in.mask));
+        pre = ld_slot(in.ring + ((tb + (unsigned)pos) & in.mask));
         if (clock64() - t0 > kWatchdogCycles) {  // a link that never delivers: report, give up
           printf("ffd long_kernel watchdog: consumer cta %d lane %d pos %d want tag %u saw %u (tb %u)\n",
                  (int)blockIdx.x, lane, pos, want, pre.y, tb);
@@ -235,11 +241,11 @@ struct LongRunner {
     In a[D], a2[D];
     int kind, kind2;
     fetch(lane, S2, a, kind);
-    uint2 pre = (has_in && lane < S2) ? ld_slot(in.ring + ((unsigned)lane & in.mask)) : none;
+    uint2 pre = (has_in && lane < S2) ? ld_slot(in.ring + ((tb + (unsigned)lane) & in.mask)) : none;
     store_elem(a, kind, lane, top_of(lane, S2, has_in, in, tb, pre), ok);
     fetch(32 + lane, S2, a, kind);
     fetch(64 + lane, S2, a2, kind2);
-    pre = (has_in && 32 + lane < S2) ? ld_slot(in.ring + ((unsigned)(32 + lane) & in.mask)) : none;
+    pre = (has_in && 32 + lane < S2) ? ld_slot(in.ring + ((tb + (unsigned)(32 + lane)) & in.mask)) : none;
     __syncwarp();
     if (has_in && lane == 0) st_ctr(in.cons, tb + (unsigned)min(32, S2));
     unsigned cons_seen = 0, cons_next = 0;
@@ -257,7 +263,7 @@ struct LongRunner {
         kind = kind2;
         fetch(2 * t + 64 + lane, S2, a2, kind2);
         const int pn = 2 * t + 32 + lane;
-        pre = (has_in && pn < S2) ? ld_slot(in.ring + ((unsigned)pn & in.mask)) : none;
+        pre = (has_in && pn < S2) ? ld_slot(in.ring + ((tb + (unsigned)pn) & in.mask)) : none;
         __syncwarp();
         if (has_in && lane == 0) st_ctr(in.cons, tb + (unsigned)min(2 * t + 32, S2));
         next_refill += 16;
@@ -292,7 +298,7 @@ struct LongRunner {
       // with one predicated 16-byte store (no divergent branch per step)
       auto one = [&](const Elem2<float, KIND, D, INT_IN>& el, int gg) {
         step2_compute<float, KIND, D, R, INT_IN>(c, diag, b0, x, el, lane);
-        st_slot2_pred(out.ring + ((2u * (unsigned)gg) & omask), b0, c[R - 1],
+        st_slot2_pred(out.ring + ((tb + 2u * (unsigned)gg) & omask), b0, c[R - 1],
                       tb + 2u * (unsigned)gg + 1u, pown & ((unsigned)gg < (unsigned)NT));
       };
 #pragma unroll 1

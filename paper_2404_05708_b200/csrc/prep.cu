@@ -11,7 +11,7 @@
 namespace ffd {
 
 __global__ void prep_keys_kernel(const int64_t* __restrict__ offsets,
-                                 const int32_t* __restrict__ lengths, int64_t B, int int_out,
+                                 const int32_t* __restrict__ lengths, int64_t B, int int_out, int long_ok,
                                  void* __restrict__ out, PairDesc* __restrict__ tmp,
                                  int16_t* __restrict__ keys, int* __restrict__ hist,
                                  int* __restrict__ long_list, int* __restrict__ long_count) {
@@ -30,7 +30,12 @@ __global__ void prep_keys_kernel(const int64_t* __restrict__ offsets,
       const int rows = swap ? m : n, cols = swap ? n : m;
       const int nb = (rows + kWarp * kMaxR - 1) / (kWarp * kMaxR);
       if (nb > kMaxBands || (nb > 1 && cols + 2 > kScratchCols)) {
-        long_list[atomicAdd(long_count, 1)] = (int)k;
+        if (long_ok) {
+          long_list[atomicAdd(long_count, 1)] = (int)k;
+        } else {  // no long-pair path for this measure (DTW): documented NaN
+          if (int_out) reinterpret_cast<long long*>(out)[k] = LLONG_MIN;
+          else reinterpret_cast<float*>(out)[k] = __int_as_float(0x7fc00000);
+        }
       } else {
         const int R = (rows + kWarp * nb - 1) / (kWarp * nb);
         PairDesc d;
@@ -86,13 +91,13 @@ __global__ void prep_scatter_kernel(const PairDesc* __restrict__ tmp,
 }
 
 cudaError_t launch_prep(const int64_t* offsets, const int32_t* lengths, int64_t B, int int_out,
-                        void* out, const BatchWs& ws, int num_sms, cudaStream_t st,
+                        int long_ok, void* out, const BatchWs& ws, int num_sms, cudaStream_t st,
                         int64_t* launches) {
   if (B == 0) return cudaSuccess;
   const int threads = 256;
   int64_t blocks = (B + threads - 1) / threads;
   if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
-  prep_keys_kernel<<<(int)blocks, threads, 0, st>>>(offsets, lengths, B, int_out, out, ws.tmp,
+  prep_keys_kernel<<<(int)blocks, threads, 0, st>>>(offsets, lengths, B, int_out, long_ok, out, ws.tmp,
                                                     ws.keys, ws.hist, ws.long_list,
                                                     ws.counters + kCtrLong);
   prep_scan_kernel<<<1, kNumKeys, 0, st>>>(ws.hist, ws.cursor, ws.counters + kCtrNumSorted);

@@ -36,7 +36,7 @@ struct BatchWs {
 };
 
 cudaError_t launch_prep(const int64_t* offsets, const int32_t* lengths, int64_t B, int int_out,
-                        void* out, const BatchWs& ws, int num_sms, cudaStream_t st,
+                        int long_ok, void* out, const BatchWs& ws, int num_sms, cudaStream_t st,
                         int64_t* launches);
 
 }  // namespace ffd

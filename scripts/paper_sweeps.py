@@ -1,0 +1,90 @@
+"""The paper's own experiment shapes on B200.
+
+E1: N curves p_i against ONE curve q (the one-vs-many batch of PAPER L259, expressed
+    through ffd_batch's offsets: every q offset is 0, no copy), N = 2^5 .. 2^14,
+    P = Q = 2^10, 2-D, steps uniform in {−1, 0, +1}², L2, fp32.
+E2: N = 2^10, P = Q = 2^5 .. 2^13 (2^14 needs the long-pair path pair by pair).
+
+For each point: GPU kernel time (CUDA events, after warm-up, as PAPER L277) and the
+CPU oracle (the plain fp64 table, OpenMP over pairs) on a bounded number of the
+same pairs — the paper's "relative improvement" axis (Fig. 1/2, whose data is
+missing from PAPER.md) restated as GPU / oracle cells/s.  Prints JSON lines.
+
+    python scripts/paper_sweeps.py [--max-exp 14] [--oracle-pairs 8]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import workload  # noqa: E402
+
+
+def one_vs_many(N, P, Q, seed_first=0):
+    """N unit-step walks of length P (p) and one of length Q (q), batch layout."""
+    cfg = workload.CONFIGS[101].scaled(pairs=N, len_p=(P, P), len_q=(Q, Q))
+    b = workload.gen_batch(cfg, first=seed_first)
+    q = b.q[:Q].copy()                       # the single reference curve
+    offsets = np.concatenate([b.offsets[:N], np.zeros(N, np.int64)])
+    return b.p, q, offsets, b.lengths
+
+
+def time_gpu(ffd, torch, p, q, off, lens, reps):
+    args = [torch.from_numpy(a).cuda() for a in (p, q, off, lens)]
+    for _ in range(3):
+        ffd.batch(*args, norm="l2")
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        out = ffd.batch(*args, norm="l2")
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps, out.cpu().numpy()
+
+
+def time_oracle(p, q, off, lens, k, threads):
+    import oracle
+    B = len(lens) // 2
+    sel = np.arange(min(k, B))
+    offs = np.concatenate([off[sel], off[B + sel]])
+    ln = np.concatenate([lens[sel], lens[B + sel]])
+    t0 = time.perf_counter()
+    ref = oracle.batch(p, q, offs, ln, 2, "l2", threads=threads)
+    return time.perf_counter() - t0, ref, sel
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--max-exp", type=int, default=14)
+    ap.add_argument("--oracle-pairs", type=int, default=16)
+    args = ap.parse_args()
+    import torch
+    import paper_2404_05708_b200 as ffd
+    ffd.lib()
+    threads = len(os.sched_getaffinity(0))
+    points = [("E1", 2 ** e, 1024, 1024) for e in range(5, args.max_exp + 1)]
+    points += [("E2", 1024, 2 ** e, 2 ** e) for e in range(5, min(args.max_exp, 13) + 1)]
+    for exp, N, P, Q in points:
+        p, q, off, lens = one_vs_many(N, P, Q)
+        cells = N * P * Q
+        ms, got = time_gpu(ffd, torch, p, q, off, lens, reps=5 if cells > 1e10 else 20)
+        k = max(1, min(N, int(args.oracle_pairs * (1024 * 1024) / (P * Q))))
+        t_cpu, ref, sel = time_oracle(p, q, off, lens, k, threads)
+        ok = bool(np.all(np.abs(got[sel] - ref) <= 1e-5 * np.abs(ref)))
+        gpu = cells / (ms * 1e-3) / 1e9
+        cpu = len(sel) * P * Q / t_cpu / 1e9
+        print(json.dumps({"exp": exp, "N": N, "P": P, "Q": Q, "cells": cells, "gpu_ms": round(ms, 4),
+                          "gpu_gcells_per_s": round(gpu, 2), "oracle_gcells_per_s": round(cpu, 3),
+                          "oracle_threads": threads, "oracle_pairs": int(len(sel)),
+                          "gpu_over_oracle": round(gpu / cpu, 1), "parity_1e-5": ok}), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -93,3 +93,15 @@ def test_config5_full_size(ffd):
     for norm, ref in gold["expected"].items():
         got = run_pairs(ffd, [(p, q)], norm)[0]
         assert abs(got - ref) <= 1e-5 * abs(ref), (norm, got, ref)
+
+
+def test_many_long_pairs_in_one_call(ffd):
+    """Successive long pairs whose streams are not a multiple of the link-ring size
+    (regression: link slots must be indexed by absolute stream position, otherwise a
+    producer already on the next pair overwrites the previous pair's last slots)."""
+    rng = np.random.default_rng(6)
+    shapes = [(2048, 2049)] * 12 + [(3000, 2600), (2047, 2100), (5000, 4099)]
+    pairs = [(walk(rng, n), walk(rng, m)) for n, m in shapes]
+    got = run_pairs(ffd, pairs, "l2")
+    for k, (p, q) in enumerate(pairs):
+        assert got[k] == oracle.pair(p, q, "l2", form="mirror"), k

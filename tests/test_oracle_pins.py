@@ -388,3 +388,32 @@ def test_dtw():
         ref = py_dtw_brute(d)   # integer-valued sums: exact
         assert oracle.dtw_table_d(d) == ref
         assert oracle.dtw_alg_d(d) == ref
+
+
+def test_dtw_pairs_pinned():
+    """Pair-level DTW (lazily evaluated d, PAPER Appendix B) against the C brute
+    force over couplings, the distance-matrix table, and closed forms; the fp32
+    mirror against fp64 within the rounding bound of a (n+m)-term sum."""
+    rng = np.random.default_rng(21)
+    for _ in range(300):
+        n, m = rng.integers(1, 7, size=2)
+        p = rand_curve(rng, n).astype(np.float32)
+        q = rand_curve(rng, m).astype(np.float32)
+        for norm in ("l1", "l2", "linf", "sql2"):
+            d = oracle.dist_matrix(p, q, norm)
+            v = oracle.dtw_pair(p, q, norm)
+            assert v == oracle.dtw_table_d(d)
+            assert abs(v - oracle.dtw_brute_d(d)) <= 1e-12 * max(1.0, abs(v))
+            assert abs(v - py_dtw_brute(d)) <= 1e-12 * max(1.0, abs(v))
+            mir = oracle.dtw_pair(p, q, norm, mirror=True)
+            assert abs(mir - v) <= (n + m + 4) * 2.0 ** -24 * abs(v) + 1e-30
+            # symmetric measure, exactly so in the fp32 mirror as well
+            assert oracle.dtw_pair(q, p, norm, mirror=True) == mir
+            # DTW(p, p) = 0; DTW ≥ δ_dF (a sum along the best coupling ≥ its max)
+            assert oracle.dtw_pair(p, p, norm) == 0.0
+            assert v >= oracle.pair(p, q, norm) - 1e-12
+    # length-1 curve: the sum of the distances to every point (a closed form)
+    p = np.array([[0.5, -1.0]], np.float32)
+    q = rand_curve(rng, 9).astype(np.float32)
+    ref = sum(float(np.hypot(*(q[j].astype(np.float64) - p[0]))) for j in range(9))
+    assert abs(oracle.dtw_pair(p, q, "l2") - ref) <= 1e-12 * ref

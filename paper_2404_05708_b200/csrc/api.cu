@@ -83,7 +83,7 @@ struct ProfScope {
   }
 };
 
-constexpr int kMaxCtasMain = 6;  // cap on resident CTAs/SM used to size scratch
+constexpr int kMaxCtasMain = 4;  // cap on resident CTAs/SM used to size scratch (= the 128-register occupancy)
 constexpr int kCtasFb = 1;
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -185,6 +185,13 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
   if (occ < 1) occ = 1;
   if (occ > kMaxCtasMain) occ = kMaxCtasMain;
   {
+    // chunk size: kChunkPairs, unless the batch is too small to give every
+    // resident warp at least one chunk (then fewer pairs per chunk)
+    const int64_t warps = (int64_t)di.sms * occ * kWarpsPerCta;
+    int64_t ch = (B + warps - 1) / warps;
+    pb.chunk = (int)(ch < 1 ? 1 : (ch > kChunkPairs ? kChunkPairs : ch));
+  }
+  {
     ProfScope prof(st, 0);
     if (main_e->launch(pb, di.sms * occ, st) != cudaSuccess) return FFD_ERR_CUDA;
   }
@@ -195,6 +202,7 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
     fb.list = ws.fb_list;
     fb.list_count = ws.counters + kCtrFb;
     fb.counter = ws.counters + kCtrChunkFb;
+    fb.chunk = kChunkPairs;
     fb.scratch = reinterpret_cast<float*>(ws.scratch_fb);
     fb.fb_list = nullptr;
     fb.fb_count = nullptr;

@@ -28,8 +28,9 @@ constexpr int kRing = 128;          // column-stream ring entries per warp (powe
 constexpr int kRingMask = kRing - 1;
 constexpr int kChunkPairs = 8;      // pairs popped per scheduling chunk
 constexpr int kMaxR = 16;           // rows per lane, single warp band = 32*kMaxR rows
-constexpr int kMaxBands = 8;        // bands per pair in the batch kernel (rows ≤ 4096)
-constexpr int kScratchCols = 2048;  // bottom-stream capacity per warp for multi-band chunks
+constexpr int kMaxBands = 16;       // bands per pair in the batch kernel (rows ≤ 8192)
+constexpr int kScratchCols = 8256;  // bottom-stream capacity per warp for multi-band chunks
+                                    // (columns ≤ 8254: the paper's E2 sweep up to 2^13 stays here)
 constexpr int kWarpsPerCta = 4;
 constexpr int kMinCtasPerSm = 4;     // caps registers at 128/thread (16 warps/SM)
 

@@ -83,7 +83,7 @@ def test_dtw_identity_and_unsupported(ffd):
 def test_dtw_too_long_is_nan(ffd):
     """no long-pair path for DTW: documented NaN (include/ffd.h)"""
     rng = np.random.default_rng(33)
-    p, q, off, lens = make(rng, [5000, 40, 6000, 50])
+    p, q, off, lens = make(rng, [9000, 40, 9500, 50])   # 9000 rows: more than 16 bands
     got = run(ffd, p, q, off, lens, "l2")
     assert np.isnan(got[0])
     assert got[1] == oracle.dtw_pair(p[off[1]:off[1] + 40], q[off[3]:off[3] + 50], "l2", mirror=True)

@@ -204,6 +204,32 @@ struct LongRunner {
     return __uint_as_float(pre.x);
   }
 
+  // Wait (lane 0 only, with backoff) until the producer has published position
+  // `pos`: it writes positions in order, so the earlier slots of the chunk are
+  // then ready too and the other lanes find their tags at the first look.  This
+  // keeps waiting warps from hammering shared memory / L2 with 32-lane polls,
+  // which slowed the producers they wait for.
+  __device__ __forceinline__ void wait_chunk(int pos, int S2, bool has_in, const Link& in,
+                                             unsigned tb) const {
+    if (has_in && lane == 0) {
+      pos = min(pos, S2 - 1);
+      const unsigned want = tb + (unsigned)pos + 1u;
+      const uint2* slot = in.ring + ((tb + (unsigned)pos) & in.mask);
+      if (ld_slot(slot).y != want) {
+        const long long t0 = clock64();
+        while (ld_slot(slot).y != want) {
+          __nanosleep(64);
+          if (clock64() - t0 > kWatchdogCycles) {
+            printf("ffd long_kernel watchdog: chunk wait cta %d pos %d want tag %u (tb %u)\n",
+                   (int)blockIdx.x, pos, want, tb);
+            break;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+
   // one band of 32·R rows starting at row r0, two columns per warp step
   // (strip.cuh warp_step2: lane ℓ at step t works on columns 2(t−ℓ), 2(t−ℓ)+1)
   __device__ bool run_band(int r0, bool has_in, Link in, bool has_out, Link out, bool last_band,
@@ -241,6 +267,7 @@ struct LongRunner {
     In a[D], a2[D];
     int kind, kind2;
     fetch(lane, S2, a, kind);
+    wait_chunk(31, S2, has_in, in, tb);
     uint2 pre = (has_in && lane < S2) ? ld_slot(in.ring + ((tb + (unsigned)lane) & in.mask)) : none;
     store_elem(a, kind, lane, top_of(lane, S2, has_in, in, tb, pre), ok);
     fetch(32 + lane, S2, a, kind);
@@ -257,6 +284,7 @@ struct LongRunner {
     int t = 0, next_refill = 16;
     while (t < total) {
       if (t == next_refill) {
+        if (2 * t < S2) wait_chunk(2 * t + 31, S2, has_in, in, tb);
         store_elem(a, kind, 2 * t + lane, top_of(2 * t + lane, S2, has_in, in, tb, pre), ok);
 #pragma unroll
         for (int cc = 0; cc < D; cc++) a[cc] = a2[cc];
@@ -276,6 +304,7 @@ struct LongRunner {
           if ((int)(cons_seen + out.mask + 1u - (tb + 2u * (unsigned)t)) <= 0) {
             const long long t0 = clock64();
             while ((int)(cons_seen + out.mask + 1u - (tb + 2u * (unsigned)t)) <= 0) {
+              __nanosleep(64);
               cons_seen = ld_ctr(out.cons);
               if (clock64() - t0 > kWatchdogCycles) {
                 printf("ffd long_kernel watchdog: producer cta %d warp %d t %d cons %u tb %u ring %u\n",
@@ -292,24 +321,25 @@ struct LongRunner {
       int g = t - lane;
       // the ring elements of the next step are loaded one step ahead (the
       // volatile link store would otherwise pin each load next to its use)
-      Elem2<float, KIND, D, INT_IN> ea, eb;
-      load_elem2<float, KIND, D, INT_IN>(ea, ring, g);
+      // software-pipelined steps (strip.cuh Pipe2): the distances of step g+1 are
+      // computed during step g's chain and the ring element of g+2 is loaded;
+      // primed again after every refill (its look-ahead may read unstored slots)
+      Pipe2<float, KIND, D, R, INT_IN> pipe;
+      pipe.prime(x, ring, g);
       // lane 31 publishes its two bottom-row values {value, tag} of every step
       // with one predicated 16-byte store (no divergent branch per step)
-      auto one = [&](const Elem2<float, KIND, D, INT_IN>& el, int gg) {
-        step2_compute<float, KIND, D, R, INT_IN>(c, diag, b0, x, el, lane);
+      auto one = [&](int gg) {
+        pipe.step(c, diag, b0, x, ring, gg, lane);
         st_slot2_pred(out.ring + ((tb + 2u * (unsigned)gg) & omask), b0, c[R - 1],
                       tb + 2u * (unsigned)gg + 1u, pown & ((unsigned)gg < (unsigned)NT));
       };
 #pragma unroll 1
       for (; t + 2 <= stop; t += 2, g += 2) {
-        load_elem2<float, KIND, D, INT_IN>(eb, ring, g + 1);
-        one(ea, g);
-        load_elem2<float, KIND, D, INT_IN>(ea, ring, g + 2);
-        one(eb, g + 1);
+        one(g);
+        one(g + 1);
       }
       if (t < stop) {
-        one(ea, g);
+        one(g);
         ++t;
       }
     }

@@ -115,6 +115,16 @@ int ffd_cdist(const void* setA, int64_t nA, int32_t lenA, const void* setB, int6
               size_t workspace_bytes, ffd_stream_t stream);
 size_t ffd_cdist_workspace_bytes(void);
 
+/* ffd_cdist_self — the same for a set against ITSELF (B = A, nB = nA):
+ *   out[(a − row_begin)*ld_out + b] = δ_dF(A_a, A_b), a ∈ [row_begin, row_end),
+ *   b ∈ [0, nA).  δ is symmetric (a metric; bit-exactly so in fp32,
+ *   DESIGN.md reading 15), so each unordered pair with both curves inside the
+ *   shard is evaluated once and written to both places: the full range costs
+ *   about half of ffd_cdist(A, A).  Same dtype/norm/workspace/stream rules.     */
+int ffd_cdist_self(const void* setA, int64_t nA, int32_t lenA, int32_t dim, int32_t norm,
+                   int32_t dtype, int64_t row_begin, int64_t row_end, void* out, int64_t ld_out,
+                   void* workspace, size_t workspace_bytes, ffd_stream_t stream);
+
 /* ---------------------------------------------------------------------------
  * ffd_validate_batch — SYNCHRONOUS device-data precondition check of a batch:
  *   lengths ≥ 1 (FFD_ERR_EMPTY), offsets+lengths within [0, np)/[0, nq)

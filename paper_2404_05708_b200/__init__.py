@@ -58,6 +58,8 @@ def lib():
         L.ffd_batch_host.restype = ctypes.c_int
         L.ffd_cdist.argtypes = [P, I64, I32_, P, I64, I32_, I32_, I32_, I32_, I64, I64, P, I64, P, SZ, P]
         L.ffd_cdist.restype = ctypes.c_int
+        L.ffd_cdist_self.argtypes = [P, I64, I32_, I32_, I32_, I32_, I64, I64, P, I64, P, SZ, P]
+        L.ffd_cdist_self.restype = ctypes.c_int
         L.ffd_cdist_workspace_bytes.argtypes = []
         L.ffd_cdist_workspace_bytes.restype = SZ
         L.ffd_validate_batch.argtypes = [P, I64, P, I64, P, P, I64, I32_, I32_, P]
@@ -76,7 +78,7 @@ def lib():
 
 
 EXPORTED = ["ffd_batch", "ffd_batch_dtw", "ffd_batch_workspace_bytes", "ffd_batch_host", "ffd_cdist",
-            "ffd_cdist_workspace_bytes", "ffd_validate_batch", "ffd_status_string",
+            "ffd_cdist_workspace_bytes", "ffd_cdist_self", "ffd_validate_batch", "ffd_status_string",
             "ffd_take_launch_count", "ffd_version", "ffd_profile_enable", "ffd_profile_take"]
 
 
@@ -207,6 +209,25 @@ def cdist(A, B, norm="l2", rows=None, out=None, ld_out=None, stream=None):
     _check(lib().ffd_cdist(A.data_ptr(), nA, lenA, B.data_ptr(), nB, lenB, dim, _norm(norm), dt, r0, r1,
                            out.data_ptr(), ld, ws.data_ptr() if ws is not None else None, wsb,
                            _stream_ptr(stream)), "ffd_cdist")
+    return out
+
+
+def cdist_self(A, norm="l2", rows=None, out=None, ld_out=None, stream=None):
+    """ffd_cdist_self: all-pairs δ of a set against itself (each unordered pair in
+    the shard evaluated once).  Returns the block [row_end-row_begin, nA]."""
+    torch = _torch()
+    dt = _dtype_code(A)
+    A = A.contiguous()
+    nA, lenA, dim = A.shape
+    r0, r1 = (0, nA) if rows is None else rows
+    ld = nA if ld_out is None else ld_out
+    if out is None:
+        out = torch.empty((r1 - r0, ld), dtype=torch.int64 if dt == I32 else torch.float32, device=A.device)
+    wsb = lib().ffd_cdist_workspace_bytes()
+    ws = workspace(wsb, A.device) if wsb else None
+    _check(lib().ffd_cdist_self(A.data_ptr(), nA, lenA, dim, _norm(norm), dt, r0, r1, out.data_ptr(), ld,
+                                ws.data_ptr() if ws is not None else None, wsb, _stream_ptr(stream)),
+           "ffd_cdist_self")
     return out
 
 

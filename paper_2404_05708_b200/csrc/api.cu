@@ -393,6 +393,37 @@ int ffd_cdist(const void* setA, int64_t nA, int32_t lenA, const void* setB, int6
   return launch_cdist(a, dev_info().sms, reinterpret_cast<cudaStream_t>(stream), &g_launches);
 }
 
+int ffd_cdist_self(const void* setA, int64_t nA, int32_t lenA, int32_t dim, int32_t norm,
+                   int32_t dtype, int64_t row_begin, int64_t row_end, void* out, int64_t ld_out,
+                   void* workspace, size_t workspace_bytes, ffd_stream_t stream) {
+  int s = check_common(dim, norm, dtype);
+  if (s) return s;
+  if (nA < 0 || row_begin < 0 || row_end < row_begin || row_end > nA) return FFD_ERR_ARG;
+  if (ld_out < nA) return FFD_ERR_ARG;
+  if (row_end == row_begin) return FFD_OK;
+  if (!setA || !out || lenA < 1) return FFD_ERR_ARG;
+  if (workspace_bytes < cdist_workspace_bytes() || (!workspace && cdist_workspace_bytes() > 0))
+    return FFD_ERR_WORKSPACE;
+  CdistArgs a{};
+  a.A = setA;
+  a.B = setA;
+  a.nA = nA;
+  a.nB = nA;
+  a.lenA = lenA;
+  a.lenB = lenA;
+  a.dim = dim;
+  a.norm = norm;
+  a.dtype = dtype;
+  a.row_begin = row_begin;
+  a.row_end = row_end;
+  a.out = out;
+  a.ld_out = ld_out;
+  a.workspace = workspace;
+  a.self = 1;
+  ProfScope prof(reinterpret_cast<cudaStream_t>(stream), 3);
+  return launch_cdist(a, dev_info().sms, reinterpret_cast<cudaStream_t>(stream), &g_launches);
+}
+
 int ffd_validate_batch(const void* p, int64_t np, const void* q, int64_t nq,
                        const int64_t* offsets, const int32_t* lengths, int64_t num_pairs,
                        int32_t dim, int32_t dtype, ffd_stream_t stream) {

@@ -39,6 +39,7 @@ struct CdistProblem {
   int* counter;
   int64_t n_items;
   int64_t tiles_b;
+  int self;  // B is A (ffd_cdist_self): evaluate each unordered pair once inside the shard
 };
 
 constexpr int kCdMinCtasPerSm = 4;  // 128 registers/thread: the W=8, R=16 shape needs ~100
@@ -68,6 +69,12 @@ __global__ void __launch_bounds__(kWarp* kWarpsPerCta, kCdMinCtasPerSm)
     const bool a_ok = a < pb.row_end;
     const int64_t b0 = tb * kCdTile;
     const int nb = (int)min((int64_t)kCdTile, pb.nB - b0);
+    if (pb.self) {
+      // every (a, b) of this item has b < a with b inside the shard: it is written
+      // by the mirror of (b, a) — skip the whole item (δ is symmetric)
+      const int64_t a_first = pb.row_begin + ablk * SEG;
+      if (b0 + nb <= a_first && b0 >= pb.row_begin) continue;
+    }
     const int S = nb * P + 1;                                  // stream positions
 
     // rows of this segment's A curve (padded by repeating the last point)
@@ -170,7 +177,11 @@ __global__ void __launch_bounds__(kWarp* kWarpsPerCta, kCdMinCtasPerSm)
         if (s == W - 1 && a_ok) {
           float v = c[R - 1];
           if constexpr (FIN == F_SQRT) v = __fsqrt_rn(v);
-          pb.out[(a - pb.row_begin) * pb.ld_out + b0 + out_b] = v;
+          const int64_t b = b0 + out_b;
+          const bool in_shard = pb.self && b >= pb.row_begin && b < pb.row_end;
+          // self mode: (a, b) with b < a inside the shard is the mirror's job
+          if (!(in_shard && b < a)) pb.out[(a - pb.row_begin) * pb.ld_out + b] = v;
+          if (in_shard && b > a) pb.out[(b - pb.row_begin) * pb.ld_out + a] = v;
         }
         ++out_b;
         next_out += P;
@@ -240,6 +251,7 @@ int launch_cdist(const CdistArgs& a, int sms, cudaStream_t st, int64_t* launches
   pb.out = reinterpret_cast<float*>(a.out);
   pb.ld_out = a.ld_out;
   pb.counter = reinterpret_cast<int*>(a.workspace);
+  pb.self = a.self;
   const int seg = kWarp / W;
   const int64_t rows = a.row_end - a.row_begin;
   pb.tiles_b = (a.nB + kCdTile - 1) / kCdTile;

@@ -13,6 +13,7 @@ struct CdistArgs {
   void* out;
   int64_t ld_out;
   void* workspace;
+  int self;  // B is A: each unordered pair inside [row_begin, row_end) evaluated once
 };
 size_t cdist_workspace_bytes();
 int launch_cdist(const CdistArgs& a, int sms, cudaStream_t st, int64_t* launches);

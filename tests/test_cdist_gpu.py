@@ -66,3 +66,23 @@ def test_config4_full_size_sampled(ffd):
     check(sel, A, B, ia, ib, "l2")
     # properties at full size: finite, non-negative, diagonal-free sanity
     assert torch.isfinite(got).all() and (got >= 0).all()
+
+
+def test_cdist_self_matches_full_and_oracle(ffd):
+    """ffd_cdist_self (each unordered pair evaluated once, mirrored) equals
+    ffd_cdist(A, A) bit for bit — δ is symmetric exactly in fp32 — on the full
+    range and on shards, with oracle spot checks."""
+    cfg = workload.CONFIGS[4].scaled(nA=300, nB=300, length=70)
+    A_h = workload.gen_set(cfg, "A")
+    A = torch.from_numpy(A_h).cuda()
+    full = ffd.cdist(A, A, "l2")
+    selfm = ffd.cdist_self(A, "l2")
+    assert torch.equal(full, selfm)
+    assert torch.equal(selfm, selfm.T)
+    assert (torch.diagonal(selfm) == 0).all()
+    for r0, r1 in [(0, 1), (37, 180), (250, 300)]:
+        blk = ffd.cdist_self(A, "l2", rows=(r0, r1))
+        assert torch.equal(blk, full[r0:r1])
+    ia = np.array([0, 5, 299, 123, 77], np.int64)
+    ib = np.array([299, 5, 0, 200, 76], np.int64)
+    check(selfm[torch.from_numpy(ia).cuda(), torch.from_numpy(ib).cuda()].cpu().numpy(), A_h, A_h, ia, ib, "l2")

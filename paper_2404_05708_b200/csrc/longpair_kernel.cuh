@@ -33,6 +33,7 @@
 #pragma once
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 
 #include "longpair.cuh"
 #include "strip.cuh"
@@ -60,7 +61,14 @@ struct LongProblem {
   uint2* gring;    // [G][kLGlobRing] slots of the link CTA g → g+1 (zeroed per call)
   unsigned* gcons; // [G] consumer progress on the link CTA g → g+1 (zeroed per call)
   int* bad;        // per long pair: a point left the fp32-exact window (int input)
+  int trace;       // FFD_LONG_TRACE=1: print each band's start/first-step/end time
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ uint2 ld_slot(const uint2* p) {
   uint2 v;
@@ -440,7 +448,10 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
 #pragma unroll
           for (int c = 0; c < D; c++) run.center[c] = (int)rows[c];
         }
+        const unsigned long long t0 = pb.trace ? gtimer() : 0ull;
         run.run_band(b * band_rows, has_in, in, has_out, out, b == nb - 1, k, pb.bad + li, tb);
+        if (pb.trace && lane == 0)
+          printf("ffdtrace band %d cta %d warp %d start %llu end %llu\n", b, cta, warp, t0, gtimer());
       };
       if (R == 4) {
         LongRunner<KIND, D, INT_IN, FIN, 4> run{rings[warp], pb, lane};
@@ -483,8 +494,9 @@ cudaError_t launch_long_k(const LongArgs& a, int sms, cudaStream_t st, const Lon
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kWarp * kLWarps, smem);
   if (occ < 1) return cudaErrorLaunchOutOfResources;
   if (G > sms * occ) G = sms * occ;
+  static const int trace = getenv("FFD_LONG_TRACE") ? atoi(getenv("FFD_LONG_TRACE")) : 0;
   LongProblem pb{a.p,      a.q,       a.offsets, a.lengths, a.num_pairs, a.list,
-                 a.list_count, a.out, w.gring,   w.gcons,   w.bad};
+                 a.list_count, a.out, w.gring,   w.gcons,   w.bad, trace};
   void* args[] = {&pb};
   return cudaLaunchCooperativeKernel((const void*)k, dim3(G), dim3(kWarp * kLWarps), args, smem, st);
 }

@@ -35,6 +35,8 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "longpair.cuh"
 #include "strip.cuh"
 
@@ -393,10 +395,20 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
   unsigned* scons = reinterpret_cast<unsigned*>(lsm + kLWarps * kLSmemRing / 2 + kLWarps * kRing * C::EW);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x, cta = blockIdx.x;
+  // Thread-block cluster: consecutive CTAs of a cluster link warp 7 → next CTA's
+  // warp 0 through DISTRIBUTED shared memory (the producer stores {value, tag}
+  // slots straight into the consumer CTA's smem ring slink[7], which warp 7 of
+  // that CTA does not use itself; the consumer publishes its progress into its
+  // own scons[7], which the producer reads remotely).  Only the link between
+  // clusters goes through L2.
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int csize = (int)cl.num_blocks(), crank = (int)cl.block_rank();
   for (int i = threadIdx.x; i < kLWarps * kLSmemRing; i += blockDim.x)
     (&slink[0][0])[i] = make_uint2(0u, 0u);
   if (threadIdx.x < kLWarps) scons[threadIdx.x] = 0u;
   __syncthreads();
+  cl.sync();  // every CTA of the cluster has initialised its rings before any remote access
   const int npairs = *pb.list_count;
   unsigned tb = 0;  // tag base: absolute stream position of the current pair on every link
   for (int li = 0; li < npairs; li++) {
@@ -425,7 +437,8 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
       // this warp does not consume its input link for this pair: its producer
       // (if any) writes nothing of it either, so mark the whole stream consumed —
       // otherwise the producer of a later pair would wait on a stale counter
-      unsigned* cons = (warp > 0) ? &scons[warp - 1] : pb.gcons + (cta + G - 1) % G;
+      unsigned* cons = (warp > 0) ? &scons[warp - 1]
+                                  : (crank > 0 ? &scons[kLWarps - 1] : pb.gcons + (cta + G - 1) % G);
       st_ctr(cons, tb + (unsigned)S);
     }
     if (b < nb) {
@@ -433,12 +446,20 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
       Link in{}, out{};
       if (warp > 0) {
         in = Link{slink[warp - 1], kLSmemRing - 1u, &scons[warp - 1]};
+      } else if (crank > 0) {  // DSMEM link from the previous CTA of this cluster
+        in = Link{slink[kLWarps - 1], kLSmemRing - 1u, &scons[kLWarps - 1]};
       } else {
         const int src = (cta + G - 1) % G;
         in = Link{pb.gring + (size_t)src * kLGlobRing, kLGlobRing - 1u, pb.gcons + src};
       }
-      if (warp < kLWarps - 1) out = Link{slink[warp], kLSmemRing - 1u, &scons[warp]};
-      else out = Link{pb.gring + (size_t)cta * kLGlobRing, kLGlobRing - 1u, pb.gcons + cta};
+      if (warp < kLWarps - 1) {
+        out = Link{slink[warp], kLSmemRing - 1u, &scons[warp]};
+      } else if (crank + 1 < csize) {  // DSMEM link into the next CTA of this cluster
+        out = Link{cl.map_shared_rank(slink[kLWarps - 1], crank + 1), kLSmemRing - 1u,
+                   cl.map_shared_rank(&scons[kLWarps - 1], crank + 1)};
+      } else {
+        out = Link{pb.gring + (size_t)cta * kLGlobRing, kLGlobRing - 1u, pb.gcons + cta};
+      }
       auto go = [&](auto& run) {
         run.n = n;
         run.m = m;
@@ -473,6 +494,7 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
     __syncthreads();
     tb += (unsigned)S;  // every link's absolute position advances by one stream per pair
   }
+  cl.sync();  // no CTA leaves while a cluster neighbour may still access its smem
 }
 
 struct LongWs {
@@ -498,6 +520,53 @@ cudaError_t launch_long_k(const LongArgs& a, int sms, cudaStream_t st, const Lon
   LongProblem pb{a.p,      a.q,       a.offsets, a.lengths, a.num_pairs, a.list,
                  a.list_count, a.out, w.gring,   w.gcons,   w.bad, trace};
   void* args[] = {&pb};
+  // clusters of 8 CTAs (DSMEM links inside a cluster), cooperative so that every
+  // CTA is co-resident; falls back to plain cooperative CTAs if the device
+  // cannot co-schedule the clusters (FFD_LONG_CLUSTER=1 forces that)
+  // cluster size: the largest of 8/4/2 whose clusters can all be co-resident
+  // for the whole grid (a smaller grid forces taller bands); FFD_LONG_CLUSTER=c
+  // forces c (1: none).
+  // Measured on config 5: clusters of 2–4 ≈ 32 ms per norm against ≈ 42 ms without
+  // (clusters of 8 fit only 128 CTAs and force R = 8).
+  static const int env_c = getenv("FFD_LONG_CLUSTER") ? atoi(getenv("FFD_LONG_CLUSTER")) : 0;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attrs[2];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  attrs[1].id = cudaLaunchAttributeCooperative;
+  attrs[1].val.cooperative = 1;
+  cfg.blockDim = dim3(kWarp * kLWarps);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attrs;
+  int best_c = 1, best_g = 0;
+  for (int csz = 8; csz >= 2; csz /= 2) {
+    if (env_c > 0 && csz != env_c) continue;
+    attrs[0].val.clusterDim.x = csz;
+    cfg.numAttrs = 1;  // the occupancy query takes the cluster shape only
+    cfg.gridDim = dim3((G / csz) * csz);
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, (const void*)k, &cfg) != cudaSuccess) {
+      (void)cudaGetLastError();
+      continue;
+    }
+    const int g = (nclusters < G / csz ? nclusters : G / csz) * csz;
+    // only a shape that keeps the whole grid: fewer CTAs would force taller bands
+    // (or leave a pair that needs every CTA without a feasible R)
+    if (g == G) {
+      best_g = g;
+      best_c = csz;
+      break;
+    }
+  }
+  if (best_c > 1 && best_g > 0) {
+    attrs[0].val.clusterDim.x = best_c;
+    cfg.gridDim = dim3(best_g);
+    cfg.numAttrs = 2;
+    if (cudaLaunchKernelExC(&cfg, (const void*)k, args) == cudaSuccess) return cudaSuccess;
+    (void)cudaGetLastError();  // clear a failed cluster launch; use the plain grid
+  }
   return cudaLaunchCooperativeKernel((const void*)k, dim3(G), dim3(kWarp * kLWarps), args, smem, st);
 }
 

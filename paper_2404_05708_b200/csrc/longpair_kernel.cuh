@@ -401,6 +401,10 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
   // that CTA does not use itself; the consumer publishes its progress into its
   // own scons[7], which the producer reads remotely).  Only the link between
   // clusters goes through L2.
+  // nothing to do (the common case of a batch without long pairs): leave before
+  // initialising 64 KB of link rings; every CTA takes the same exit, so no
+  // cluster barrier is left waiting
+  if (*pb.list_count == 0) return;
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   const int csize = (int)cl.num_blocks(), crank = (int)cl.block_rank();
@@ -511,9 +515,18 @@ cudaError_t launch_long_k(const LongArgs& a, int sms, cudaStream_t st, const Lon
   using C = SCfg<float, KIND, D, INT_IN>;
   const size_t smem = sizeof(uint2) * kLWarps * kLSmemRing + sizeof(uint4) * kLWarps * kRing * C::EW +
                       sizeof(unsigned) * kLWarps;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kWarp * kLWarps, smem);
+  // per-device caches: attribute, occupancy and the cluster shape for this grid
+  // (the host-side queries would otherwise cost tens of µs on every call)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static int occ_cache[64] = {0};
+  static int clu_cache_g[64] = {0}, clu_cache_c[64] = {0}, clu_cache_bg[64] = {0};
+  int occ = dev < 64 ? occ_cache[dev] : 0;
+  if (occ == 0) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kWarp * kLWarps, smem);
+    if (dev < 64) occ_cache[dev] = occ;
+  }
   if (occ < 1) return cudaErrorLaunchOutOfResources;
   if (G > sms * occ) G = sms * occ;
   static const int trace = getenv("FFD_LONG_TRACE") ? atoi(getenv("FFD_LONG_TRACE")) : 0;
@@ -541,7 +554,12 @@ cudaError_t launch_long_k(const LongArgs& a, int sms, cudaStream_t st, const Lon
   cfg.stream = st;
   cfg.attrs = attrs;
   int best_c = 1, best_g = 0;
-  for (int csz = 8; csz >= 2; csz /= 2) {
+  const bool cached = dev < 64 && clu_cache_g[dev] == G && clu_cache_c[dev] > 0;
+  if (cached) {
+    best_c = clu_cache_c[dev];
+    best_g = clu_cache_bg[dev];
+  }
+  for (int csz = 8; csz >= 2 && !cached; csz /= 2) {
     if (env_c > 0 && csz != env_c) continue;
     attrs[0].val.clusterDim.x = csz;
     cfg.numAttrs = 1;  // the occupancy query takes the cluster shape only
@@ -559,6 +577,11 @@ cudaError_t launch_long_k(const LongArgs& a, int sms, cudaStream_t st, const Lon
       best_c = csz;
       break;
     }
+  }
+  if (!cached && dev < 64) {
+    clu_cache_g[dev] = G;
+    clu_cache_c[dev] = best_c;
+    clu_cache_bg[dev] = best_g;
   }
   if (best_c > 1 && best_g > 0) {
     attrs[0].val.clusterDim.x = best_c;

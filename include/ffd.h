@@ -108,6 +108,9 @@ int ffd_batch_host(const void* p_host, int64_t np, const void* q_host, int64_t n
  *   out: float (FFD_F32) or int64 (FFD_I32), ld_out ≥ nB elements.
  *   [row_begin, row_end) is the caller's shard (one rank's block of rows).
  *   workspace: ≥ ffd_cdist_workspace_bytes() bytes (may be NULL if that is 0).
+ *   fp32 input with dim 2–3 and lenA ≤ 512 runs the dedicated all-pairs kernel;
+ *   every other dtype/dim/length is evaluated as chunked batches of (a, b)
+ *   pairs by ffd_batch's kernels (scratch from the stream-ordered pool).
  * ------------------------------------------------------------------------- */
 int ffd_cdist(const void* setA, int64_t nA, int32_t lenA, const void* setB, int64_t nB,
               int32_t lenB, int32_t dim, int32_t norm, int32_t dtype, int64_t row_begin,

@@ -231,6 +231,77 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
   return FFD_OK;
 }
 
+// ---- all-pairs shapes the dedicated cdist kernel does not cover -------------
+// (int32 input, dim 1 or 4, A-curves longer than 512 points): the block is
+// evaluated as chunked batches of (a, b) pairs by the batch kernels.  Pair lists
+// are generated on the device; scratch comes from the stream-ordered pool.
+__global__ void cdist_pairs_kernel(int64_t first, int64_t n, int64_t row_begin, int64_t nB,
+                                   int32_t lenA, int32_t lenB, int64_t* offsets,
+                                   int32_t* lengths) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t idx = first + k;
+    const int64_t a = row_begin + idx / nB, b = idx % nB;
+    offsets[k] = a * lenA;
+    offsets[n + k] = b * lenB;
+    lengths[k] = lenA;
+    lengths[n + k] = lenB;
+  }
+}
+
+template <typename O>
+__global__ void cdist_scatter_kernel(int64_t first, int64_t n, int64_t nB, const O* src, O* out,
+                                     int64_t ld_out) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t idx = first + k;
+    out[(idx / nB) * ld_out + idx % nB] = src[k];
+  }
+}
+
+static int cdist_via_batch(const CdistArgs& a, cudaStream_t st) {
+  const int64_t rows = a.row_end - a.row_begin;
+  const int64_t total = rows * a.nB;
+  const int64_t CH = total < (int64_t)(1 << 20) ? total : (int64_t)(1 << 20);
+  const size_t osz = a.dtype == FFD_I32 ? 8 : 4;
+  const size_t wsb = batch_layout(nullptr, CH, dev_info().sms).bytes;
+  const size_t off_b = (size_t)CH * 2 * sizeof(int64_t), len_b = (size_t)CH * 2 * sizeof(int32_t);
+  char* buf = nullptr;
+  const size_t total_b = off_b + len_b + (size_t)CH * osz + wsb + 1024;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&buf), total_b, st) != cudaSuccess) return FFD_ERR_CUDA;
+  int64_t* offsets = reinterpret_cast<int64_t*>(buf);
+  int32_t* lengths = reinterpret_cast<int32_t*>(buf + off_b);
+  char* tmp = buf + ((off_b + len_b + 255) / 256) * 256;
+  char* ws = tmp + (((size_t)CH * osz + 255) / 256) * 256;
+  int rc = FFD_OK;
+  for (int64_t first = 0; first < total && rc == FFD_OK; first += CH) {
+    const int64_t n = (total - first < CH) ? total - first : CH;
+    const int blocks = (int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
+    cdist_pairs_kernel<<<blocks, 256, 0, st>>>(first, n, a.row_begin, a.nB, a.lenA, a.lenB, offsets,
+                                               lengths);
+    ++g_launches;
+    rc = batch_impl(a.A, a.B, offsets, lengths, n, a.dim, a.norm, a.dtype, tmp, ws, wsb, st);
+    if (rc != FFD_OK) break;
+    if (osz == 8)
+      cdist_scatter_kernel<long long><<<blocks, 256, 0, st>>>(
+          first, n, a.nB, reinterpret_cast<const long long*>(tmp), reinterpret_cast<long long*>(a.out),
+          a.ld_out);
+    else
+      cdist_scatter_kernel<float><<<blocks, 256, 0, st>>>(first, n, a.nB, reinterpret_cast<const float*>(tmp),
+                                                          reinterpret_cast<float*>(a.out), a.ld_out);
+    ++g_launches;
+    if (cudaGetLastError() != cudaSuccess) rc = FFD_ERR_CUDA;
+  }
+  cudaFreeAsync(buf, st);
+  return rc;
+}
+
+static int cdist_dispatch(const CdistArgs& a, cudaStream_t st) {
+  const int rc = launch_cdist(a, dev_info().sms, st, &g_launches);
+  if (rc != FFD_ERR_UNSUPPORTED) return rc;
+  return cdist_via_batch(a, st);  // shapes outside the dedicated kernel
+}
+
 }  // namespace ffd
 
 using namespace ffd;
@@ -390,7 +461,7 @@ int ffd_cdist(const void* setA, int64_t nA, int32_t lenA, const void* setB, int6
   a.ld_out = ld_out;
   a.workspace = workspace;
   ProfScope prof(reinterpret_cast<cudaStream_t>(stream), 3);
-  return launch_cdist(a, dev_info().sms, reinterpret_cast<cudaStream_t>(stream), &g_launches);
+  return cdist_dispatch(a, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int ffd_cdist_self(const void* setA, int64_t nA, int32_t lenA, int32_t dim, int32_t norm,
@@ -421,7 +492,7 @@ int ffd_cdist_self(const void* setA, int64_t nA, int32_t lenA, int32_t dim, int3
   a.workspace = workspace;
   a.self = 1;
   ProfScope prof(reinterpret_cast<cudaStream_t>(stream), 3);
-  return launch_cdist(a, dev_info().sms, reinterpret_cast<cudaStream_t>(stream), &g_launches);
+  return cdist_dispatch(a, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int ffd_validate_batch(const void* p, int64_t np, const void* q, int64_t nq,

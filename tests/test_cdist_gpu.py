@@ -86,3 +86,46 @@ def test_cdist_self_matches_full_and_oracle(ffd):
     ia = np.array([0, 5, 299, 123, 77], np.int64)
     ib = np.array([299, 5, 0, 200, 76], np.int64)
     check(selfm[torch.from_numpy(ia).cuda(), torch.from_numpy(ib).cuda()].cpu().numpy(), A_h, A_h, ia, ib, "l2")
+
+
+def _dense_pairs(A, B, r0, r1):
+    """oracle batch layout of all (a, b), a ∈ [r0, r1), over the flattened sets"""
+    nA, LA, dim = A.shape
+    nB, LB, _ = B.shape
+    a = np.repeat(np.arange(r0, r1), nB)
+    b = np.tile(np.arange(nB), r1 - r0)
+    off = np.concatenate([a * LA, b * LB]).astype(np.int64)
+    lens = np.concatenate([np.full(len(a), LA), np.full(len(b), LB)]).astype(np.int32)
+    return A.reshape(-1, dim), B.reshape(-1, dim), off, lens
+
+
+@pytest.mark.parametrize("dim,dtype,lenA,lenB,norm", [
+    (1, "f", 40, 50, "l2"), (4, "f", 30, 33, "l1"), (2, "f", 700, 90, "l2"),
+    (2, "i", 60, 70, "sql2"), (3, "i", 45, 20, "linf")])
+def test_cdist_general_shapes(ffd, dim, dtype, lenA, lenB, norm):
+    """shapes outside the dedicated all-pairs kernel (int32, dim 1/4, A-curves
+    longer than 512 points) go through the batch kernels: same results"""
+    rng = np.random.default_rng(dim * 100 + lenA)
+    nA, nB = 9, 7
+    if dtype == "i":
+        A = np.cumsum(rng.integers(-8, 9, size=(nA, lenA, dim)), 1).astype(np.int32)
+        B = np.cumsum(rng.integers(-8, 9, size=(nB, lenB, dim)), 1).astype(np.int32)
+    else:
+        A = np.cumsum(rng.normal(size=(nA, lenA, dim)), 1).astype(np.float32)
+        B = np.cumsum(rng.normal(size=(nB, lenB, dim)), 1).astype(np.float32)
+    got = ffd.cdist(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), norm, rows=(2, 8)).cpu().numpy()
+    p, q, off, lens = _dense_pairs(A, B, 2, 8)
+    if dtype == "i":
+        ref = oracle.batch(p, q, off, lens, dim, norm).reshape(6, nB)
+        assert np.array_equal(got, ref)
+    else:
+        mir = oracle.batch(p, q, off, lens, dim, norm, mirror=True).reshape(6, nB)
+        assert np.array_equal(got, mir)
+
+
+def test_cdist_self_general_shape(ffd):
+    rng = np.random.default_rng(8)
+    A = np.cumsum(rng.normal(size=(11, 600, 2)), 1).astype(np.float32)   # > 512 points
+    got = ffd.cdist_self(torch.from_numpy(A).cuda(), "l2").cpu().numpy()
+    p, q, off, lens = _dense_pairs(A, A, 0, 11)
+    assert np.array_equal(got, oracle.batch(p, q, off, lens, 2, "l2", mirror=True).reshape(11, 11))

@@ -344,9 +344,11 @@ def bench_ffd(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32" if cfg.dtype == "f32" else "f32-exact-int",
+        "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
         "config": {"workload": cfg.name, "pairs_per_gpu": B, "cells_per_gpu_step": cells,
+                   "arithmetic": ("fp32 arithmetic, exact for these integers (every partial < 2^24), "
+                                  "int64 results" if cfg.dtype == "i32" else "fp32"),
                    "dim": cfg.dim, "norm": cfg.norm, "lengths": list(cfg.len_p),
                    "l2": "inputs larger than L2 (%.0f MB per GPU)" % ((b.p.nbytes + b.q.nbytes) / 1e6),
                    "parallelism": f"pairs sharded over {ws} GPU(s), no collective on the data path"},

@@ -73,11 +73,12 @@ def _declare(L):
     L.orc_frechet_full_table_d.restype = None
     L.orc_frechet_full_table_d.argtypes = [_P, _I64, _I64, _P]
     for n in ("orc_pair_f32", "orc_pair_linear_f32", "orc_pair_i32", "orc_pair_linear_i32",
-              "orc_pair_f32mirror", "orc_pair_dtw_f32", "orc_pair_dtw_f32mirror"):
+              "orc_pair_f32mirror", "orc_pair_dtw_f32", "orc_pair_dtw_f32mirror",
+              "orc_pair_dist_sum_f32"):
         getattr(L, n).restype = _INT
         getattr(L, n).argtypes = [_P, _I64, _P, _I64, _INT, _INT, _P]
     for n in ("orc_batch_f32", "orc_batch_f32mirror", "orc_batch_i32", "orc_batch_dtw_f32",
-              "orc_batch_dtw_f32mirror"):
+              "orc_batch_dtw_f32mirror", "orc_batch_dist_sum_f32"):
         getattr(L, n).restype = _INT
         getattr(L, n).argtypes = [_P, _P, _P, _P, _I64, _INT, _INT, _P, _INT]
     for n in ("orc_cdist_entries_f32", "orc_cdist_entries_f32mirror"):
@@ -202,6 +203,31 @@ def dtw_batch(p, q, offsets, lengths, dim, norm="l2", threads=0, mirror=False, c
     out = np.empty(B, np.float32 if mirror else np.float64)
     fn = lib().orc_batch_dtw_f32mirror if mirror else lib().orc_batch_dtw_f32
     st = fn(_ptr(p), _ptr(q), _ptr(offsets), _ptr(lengths), B, dim, _norm(norm), _ptr(out), threads)
+    if st and check:
+        raise OracleError(st)
+    return out
+
+
+def dist_sum_pair(p, q, norm="l2"):
+    """Σ_ij d(p_i, q_j) of float32 curves in fp64."""
+    p, q = _c(p, np.float32), _c(q, np.float32)
+    out = np.zeros(1, np.float64)
+    st = lib().orc_pair_dist_sum_f32(_ptr(p), p.shape[0], _ptr(q), q.shape[0], p.shape[1],
+                                     _norm(norm), _ptr(out))
+    if st:
+        raise OracleError(st)
+    return out[0].item()
+
+
+def dist_sum_batch(p, q, offsets, lengths, dim, norm="l2", threads=0, check=True):
+    """Σ_ij d_ij of every pair of a batch (float32 curves), layout as batch()."""
+    offsets = _c(offsets, np.int64)
+    lengths = _c(lengths, np.int32)
+    B = offsets.shape[0] // 2
+    p, q = _c(p, np.float32), _c(q, np.float32)
+    out = np.empty(B, np.float64)
+    st = lib().orc_batch_dist_sum_f32(_ptr(p), _ptr(q), _ptr(offsets), _ptr(lengths), B, dim,
+                                      _norm(norm), _ptr(out), threads)
     if st and check:
         raise OracleError(st)
     return out

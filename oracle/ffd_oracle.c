@@ -734,3 +734,37 @@ int orc_batch_dtw_f32mirror(const float* p, const float* q, const int64_t* offse
   }
   return first;
 }
+
+/* ---- Σ_ij d_ij ------------------------------------- */
+int orc_pair_dist_sum_f32(const float* p, int64_t P, const float* q, int64_t Q, int dim, int norm,
+                          double* out) {
+  int st = check_norm_f(dim, norm);
+  if (st) return st;
+  if (P < 1 || Q < 1) return ORC_ERR_EMPTY;
+  if (check_finite(p, P, dim) || check_finite(q, Q, dim)) return ORC_ERR_NONFINITE;
+  double s = 0.0;
+  for (int64_t i = 0; i < P; i++)
+    for (int64_t j = 0; j < Q; j++) s += orc_point_dist_f32(p + i * dim, q + j * dim, dim, norm);
+  *out = s;
+  return ORC_OK;
+}
+
+int orc_batch_dist_sum_f32(const float* p, const float* q, const int64_t* offsets,
+                           const int32_t* lengths, int64_t B, int dim, int norm, double* out,
+                           int threads) {
+  int first = ORC_OK;
+  int nt = threads_or_default(threads);
+  (void)nt;
+#pragma omp parallel for schedule(dynamic, 8) num_threads(nt)
+  for (int64_t k = 0; k < B; k++) {
+    double r = NAN;
+    int st = orc_pair_dist_sum_f32(p + offsets[k] * dim, lengths[k], q + offsets[B + k] * dim,
+                                   lengths[B + k], dim, norm, &r);
+    out[k] = st ? NAN : r;
+    if (st) {
+#pragma omp critical
+      if (first == ORC_OK) first = st;
+    }
+  }
+  return first;
+}

@@ -126,6 +126,17 @@ int orc_batch_dtw_f32mirror(const float* p, const float* q, const int64_t* offse
                             const int32_t* lengths, int64_t B, int dim, int norm, float* out,
                             int threads);
 
+/* ---- Σ_ij d_ij: the paper's "upper limit" baseline --
+ * The sum over all P·Q point distances of a pair, with the same d_ij as the DP
+ * (L2 = sqrt per cell, the paper's hypot workload L271), in fp64 in row-major
+ * order.  It is what the paper's SIMD DP "comes close" to: the cost of the
+ * distances alone, without the recurrence. */
+int orc_pair_dist_sum_f32(const float* p, int64_t P, const float* q, int64_t Q, int dim, int norm,
+                          double* out);
+int orc_batch_dist_sum_f32(const float* p, const float* q, const int64_t* offsets,
+                           const int32_t* lengths, int64_t B, int dim, int norm, double* out,
+                           int threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -417,3 +417,49 @@ def test_dtw_pairs_pinned():
     q = rand_curve(rng, 9).astype(np.float32)
     ref = sum(float(np.hypot(*(q[j].astype(np.float64) - p[0]))) for j in range(9))
     assert abs(oracle.dtw_pair(p, q, "l2") - ref) <= 1e-12 * ref
+
+
+def test_dist_sum_pinned():
+    """Σ_ij d_ij (the paper's "upper limit" baseline)
+    against closed forms that a dropped term, a wrong index or a wrong norm
+    breaks, and against DTW with a one-point curve (Appendix B: the only
+    coupling visits every q_j once, so DTW = Σ_j d_0j)."""
+    # 1-D integer walks p_i = i, q_j = j: every norm is |i − j|.
+    for n in (1, 2, 7, 33):
+        p = np.arange(n, dtype=np.float32)[:, None]
+        s_abs = n * (n * n - 1) / 3          # Σ_{i,j<n} |i − j|
+        s_sq = n * n * (n * n - 1) / 6       # Σ_{i,j<n} (i − j)²
+        for norm, ref in (("l1", s_abs), ("l2", s_abs), ("linf", s_abs), ("sql2", s_sq)):
+            assert oracle.dist_sum_pair(p, p, norm) == ref
+    # 3-4-5 triangles: p = {(0,0)}, q_j = (3j, 4j), j < m
+    for m in (1, 5, 40):
+        j = np.arange(m, dtype=np.float64)
+        q = np.stack([3 * j, 4 * j], 1).astype(np.float32)
+        p = np.zeros((1, 2), np.float32)
+        for norm, ref in (("l2", 5 * j.sum()), ("l1", 7 * j.sum()), ("linf", 4 * j.sum()),
+                          ("sql2", 25 * (j * j).sum())):
+            assert oracle.dist_sum_pair(p, q, norm) == ref
+            assert oracle.dist_sum_pair(q, p, norm) == ref
+    # unequal lengths, 1-D: p_i = i (n points), q_j = j (m points), sql2
+    n, m = 5, 9
+    ref = sum((i - j) ** 2 for i in range(n) for j in range(m))
+    assert oracle.dist_sum_pair(np.arange(n, dtype=np.float32)[:, None],
+                                np.arange(m, dtype=np.float32)[:, None], "sql2") == ref
+    rng = np.random.default_rng(5)
+    for _ in range(50):
+        m = int(rng.integers(1, 12))
+        p = rand_curve(rng, 1).astype(np.float32)
+        q = rand_curve(rng, m).astype(np.float32)
+        for norm in ("l1", "l2", "linf", "sql2"):
+            v = oracle.dist_sum_pair(p, q, norm)
+            assert abs(v - oracle.dtw_pair(p, q, norm)) <= 1e-12 * max(1.0, v)
+    # batch == pairs (one-vs-many layout: every q offset 0)
+    B = 6
+    lens = rng.integers(1, 20, size=2 * B).astype(np.int32)
+    lens[B:] = lens[B]
+    P = rand_curve(rng, int(lens[:B].sum())).astype(np.float32)
+    Q = rand_curve(rng, int(lens[B])).astype(np.float32)
+    offs = np.concatenate([np.concatenate([[0], np.cumsum(lens[:B])[:-1]]), np.zeros(B)]).astype(np.int64)
+    got = oracle.dist_sum_batch(P, Q, offs, lens, 2, "l2")
+    for k in range(B):
+        assert got[k] == oracle.dist_sum_pair(P[offs[k]:offs[k] + lens[k]], Q, "l2")

@@ -92,6 +92,19 @@ int ffd_batch_dtw(const void* p, const void* q, const int64_t* offsets, const in
                   int64_t num_pairs, int32_t dim, int32_t norm, int32_t dtype, void* out,
                   void* workspace, size_t workspace_bytes, ffd_stream_t stream);
 
+/* ffd_dist_sum — Σ_i Σ_j d(p_i, q_j) of each of B pairs: the paper's "upper
+ *   limit" baseline, the distances of the DP workload
+ *   (FFD_L2 takes a square root per cell, the paper's hypot L271) without the
+ *   recurrence.  A calibration kernel: how close the DP comes to the cost of
+ *   its distances alone.  Layout, offsets (one-vs-many allowed) and stream
+ *   semantics as ffd_batch; dtype must be FFD_F32 (FFD_ERR_UNSUPPORTED
+ *   otherwise); out: double[B], deterministic (fixed summation order), relative
+ *   error ≤ (35 + 2·dim)·2⁻²⁴ of the exact sum; NaN for a pair with a length
+ *   < 1.  Needs no workspace (scratch from the stream-ordered pool).          */
+int ffd_dist_sum(const void* p, const void* q, const int64_t* offsets, const int32_t* lengths,
+                 int64_t num_pairs, int32_t dim, int32_t norm, int32_t dtype, double* out,
+                 ffd_stream_t stream);
+
 /* ffd_batch_host — the same computation from HOST buffers (end-to-end path).
  *   p_host: [np, dim], q_host: [nq, dim]; offsets_host/lengths_host as above;
  *   out_host: float[B] / int64[B].  Host buffers should be pinned for overlap.

@@ -8,6 +8,7 @@ missing, calls raise.
 
     batch(p, q, offsets, lengths, norm)        -> Tensor[B]   (ffd_batch)
     dtw_batch(p, q, offsets, lengths, norm)    -> Tensor[B]   (ffd_batch_dtw)
+    dist_sum(p, q, offsets, lengths, norm)     -> Tensor[B] f64 (ffd_dist_sum)
     batch_host(p, q, offsets, lengths, norm)   -> ndarray[B]  (ffd_batch_host)
     cdist(A, B, norm, rows=None)               -> Tensor      (ffd_cdist)
     validate(p, q, offsets, lengths)           -> status      (ffd_validate_batch)
@@ -52,6 +53,8 @@ def lib():
         L.ffd_batch.restype = ctypes.c_int
         L.ffd_batch_dtw.argtypes = [P, P, P, P, I64, I32_, I32_, I32_, P, P, SZ, P]
         L.ffd_batch_dtw.restype = ctypes.c_int
+        L.ffd_dist_sum.argtypes = [P, P, P, P, I64, I32_, I32_, I32_, P, P]
+        L.ffd_dist_sum.restype = ctypes.c_int
         L.ffd_batch_workspace_bytes.argtypes = [I64]
         L.ffd_batch_workspace_bytes.restype = SZ
         L.ffd_batch_host.argtypes = [P, I64, P, I64, P, P, I64, I32_, I32_, I32_, P, P]
@@ -77,7 +80,7 @@ def lib():
     return _lib
 
 
-EXPORTED = ["ffd_batch", "ffd_batch_dtw", "ffd_batch_workspace_bytes", "ffd_batch_host", "ffd_cdist",
+EXPORTED = ["ffd_batch", "ffd_batch_dtw", "ffd_dist_sum", "ffd_batch_workspace_bytes", "ffd_batch_host", "ffd_cdist",
             "ffd_cdist_workspace_bytes", "ffd_cdist_self", "ffd_validate_batch", "ffd_status_string",
             "ffd_take_launch_count", "ffd_version", "ffd_profile_enable", "ffd_profile_take"]
 
@@ -172,6 +175,24 @@ def batch(p, q, offsets, lengths, norm="l2", out=None, stream=None, measure="fre
 def dtw_batch(p, q, offsets, lengths, norm="l2", out=None, stream=None):
     """Dynamic time warping of B pairs (ffd_batch_dtw): same layout as batch()."""
     return batch(p, q, offsets, lengths, norm=norm, out=out, stream=stream, measure="dtw")
+
+
+def dist_sum(p, q, offsets, lengths, norm="l2", out=None, stream=None):
+    """Σ_ij d(p_i, q_j) of B pairs (ffd_dist_sum, the paper's "upper limit"
+    baseline): same layout as batch(), float32 curves, float64 result."""
+    torch = _torch()
+    if _dtype_code(p) != F32:
+        raise FFDError(-2, "ffd_dist_sum")
+    p, q = p.contiguous(), q.contiguous()
+    offsets = offsets.contiguous()
+    lengths = lengths.contiguous()
+    B = offsets.shape[0] // 2
+    if out is None:
+        out = torch.empty(B, dtype=torch.float64, device=p.device)
+    _check(lib().ffd_dist_sum(p.data_ptr(), q.data_ptr(), offsets.data_ptr(), lengths.data_ptr(), B,
+                              p.shape[1], _norm(norm), F32, out.data_ptr(), _stream_ptr(stream)),
+           "ffd_dist_sum")
+    return out
 
 
 def batch_host(p: np.ndarray, q: np.ndarray, offsets: np.ndarray, lengths: np.ndarray, norm="l2",

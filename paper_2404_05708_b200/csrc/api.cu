@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "cdist.cuh"
+#include "distsum.cuh"
 #include "ffd.h"
 #include "longpair.cuh"
 #include "prep.cuh"
@@ -379,6 +380,20 @@ int ffd_batch_dtw(const void* p, const void* q, const int64_t* offsets, const in
                   void* workspace, size_t workspace_bytes, ffd_stream_t stream) {
   return batch_impl(p, q, offsets, lengths, num_pairs, dim, norm, dtype, out, workspace,
                     workspace_bytes, reinterpret_cast<cudaStream_t>(stream), 1);
+}
+
+int ffd_dist_sum(const void* p, const void* q, const int64_t* offsets, const int32_t* lengths,
+                 int64_t num_pairs, int32_t dim, int32_t norm, int32_t dtype, double* out,
+                 ffd_stream_t stream) {
+  int s = check_common(dim, norm, dtype);
+  if (s) return s;
+  if (dtype != FFD_F32) return FFD_ERR_UNSUPPORTED;
+  if (num_pairs < 0) return FFD_ERR_ARG;
+  if (num_pairs == 0) return FFD_OK;
+  if (!p || !q || !offsets || !lengths || !out) return FFD_ERR_ARG;
+  return launch_dist_sum(static_cast<const float*>(p), static_cast<const float*>(q), offsets,
+                         lengths, num_pairs, dim, norm, out, dev_info().sms,
+                         reinterpret_cast<cudaStream_t>(stream), &g_launches);
 }
 
 int ffd_batch_host(const void* p_host, int64_t np, const void* q_host, int64_t nq,

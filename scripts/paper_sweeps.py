@@ -5,7 +5,9 @@ E1: N curves p_i against ONE curve q (the one-vs-many batch of PAPER L259, expre
     P = Q = 2^10, 2-D, steps uniform in {−1, 0, +1}², L2, fp32.
 E2: N = 2^10, P = Q = 2^5 .. 2^13 (2^14 needs the long-pair path pair by pair).
 
-For each point: GPU kernel time (CUDA events, after warm-up, as PAPER L277) and the
+For each point: the Σ_ij d_ij "upper limit" kernel (ffd_dist_sum, PAPER L300,
+L304–L305) timed beside the DP, with a root per cell (the paper's hypot) and
+without (the DP's own squared distance); GPU kernel time (CUDA events, after warm-up, as PAPER L277) and the
 CPU oracle (the plain fp64 table, OpenMP over pairs) on a bounded number of the
 same pairs — the paper's "relative improvement" axis (Fig. 1/2, whose data is
 missing from PAPER.md) restated as GPU / oracle cells/s.  Prints JSON lines.
@@ -35,15 +37,16 @@ def one_vs_many(N, P, Q, seed_first=0):
     return b.p, q, offsets, b.lengths
 
 
-def time_gpu(ffd, torch, p, q, off, lens, reps):
+def time_gpu(ffd, torch, p, q, off, lens, reps, fn="batch", norm="l2"):
     args = [torch.from_numpy(a).cuda() for a in (p, q, off, lens)]
+    call = getattr(ffd, fn)
     for _ in range(3):
-        ffd.batch(*args, norm="l2")
+        call(*args, norm=norm)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(reps):
-        out = ffd.batch(*args, norm="l2")
+        out = call(*args, norm=norm)
     e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / reps, out.cpu().numpy()
@@ -80,10 +83,23 @@ def main():
         ok = bool(np.all(np.abs(got[sel] - ref) <= 1e-5 * np.abs(ref)))
         gpu = cells / (ms * 1e-3) / 1e9
         cpu = len(sel) * P * Q / t_cpu / 1e9
+        # the paper's "upper limit": Σ_ij d_ij alone, with
+        # a root per cell (its hypot workload) and without (the DP's own d here)
+        reps = 5 if cells > 1e10 else 20
+        ms_l2, s_l2 = time_gpu(ffd, torch, p, q, off, lens, reps, "dist_sum", "l2")
+        ms_sq, _ = time_gpu(ffd, torch, p, q, off, lens, reps, "dist_sum", "sql2")
+        import oracle
+        offs = np.concatenate([off[sel[:2]], off[N + sel[:2]]])
+        ln = np.concatenate([lens[sel[:2]], lens[N + sel[:2]]])
+        ref_s = oracle.dist_sum_batch(p, q, offs, ln, 2, "l2")
+        ok_s = bool(np.all(np.abs(s_l2[sel[:2]] - ref_s) <= 39 * 2.0 ** -24 * ref_s))
         print(json.dumps({"exp": exp, "N": N, "P": P, "Q": Q, "cells": cells, "gpu_ms": round(ms, 4),
                           "gpu_gcells_per_s": round(gpu, 2), "oracle_gcells_per_s": round(cpu, 3),
                           "oracle_threads": threads, "oracle_pairs": int(len(sel)),
-                          "gpu_over_oracle": round(gpu / cpu, 1), "parity_1e-5": ok}), flush=True)
+                          "gpu_over_oracle": round(gpu / cpu, 1), "parity_1e-5": ok,
+                          "sumd_l2_gcells_per_s": round(cells / (ms_l2 * 1e-3) / 1e9, 2),
+                          "sumd_sql2_gcells_per_s": round(cells / (ms_sq * 1e-3) / 1e9, 2),
+                          "dp_over_sumd_sql2": round(ms_sq / ms, 3), "sumd_parity": ok_s}), flush=True)
 
 
 if __name__ == "__main__":

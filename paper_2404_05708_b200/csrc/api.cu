@@ -131,7 +131,8 @@ static int check_common(int32_t dim, int32_t norm, int32_t dtype) {
 // measure: 0 discrete Fréchet (Eq. (1)), 1 DTW (Appendix B)
 static int batch_impl(const void* p, const void* q, const int64_t* offsets, const int32_t* lengths,
                       int64_t B, int32_t dim, int32_t norm, int32_t dtype, void* out,
-                      void* workspace, size_t ws_bytes, cudaStream_t st, int measure = 0) {
+                      void* workspace, size_t ws_bytes, cudaStream_t st, int measure = 0,
+                      bool long_possible = true) {
   int s = check_common(dim, norm, dtype);
   if (s) return s;
   if (measure == 1 && dtype != FFD_F32) return FFD_ERR_UNSUPPORTED;
@@ -159,11 +160,6 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
     if (!fb_e) return FFD_ERR_UNSUPPORTED;
   }
 
-  // zero counters + histogram (one memset of the leading block)
-  if (cudaMemsetAsync(ws.counters, 0,
-                      reinterpret_cast<char*>(ws.cursor) - reinterpret_cast<char*>(ws.counters),
-                      st) != cudaSuccess)
-    return FFD_ERR_CUDA;
   if (launch_prep(offsets, lengths, B, int_in, measure == 0, out, ws, di.sms, st, &g_launches) !=
       cudaSuccess)
     return FFD_ERR_CUDA;
@@ -194,7 +190,12 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
   }
   {
     ProfScope prof(st, 0);
-    if (main_e->launch(pb, di.sms * occ, st) != cudaSuccess) return FFD_ERR_CUDA;
+    // no more CTAs than there are chunks to take (a small batch would otherwise
+    // start hundreds of CTAs that only find the chunk counter exhausted)
+    const int64_t chunks = (B + pb.chunk - 1) / pb.chunk;
+    const int64_t need = (chunks + kWarpsPerCta - 1) / kWarpsPerCta;
+    const int ctas = (int)(need < (int64_t)di.sms * occ ? need : (int64_t)di.sms * occ);
+    if (main_e->launch(pb, ctas, st) != cudaSuccess) return FFD_ERR_CUDA;
   }
   ++g_launches;
 
@@ -214,6 +215,7 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
   }
 
   if (measure != 0) return FFD_OK;  // DTW: no long-pair path (prep wrote NaN for those pairs)
+  if (!long_possible) return FFD_OK;  // the caller saw every length: no pair is long
   // pairs too long for the band scratch of the batch kernel: cross-CTA wavefront
   LongArgs la{};
   la.p = p;
@@ -281,7 +283,8 @@ static int cdist_via_batch(const CdistArgs& a, cudaStream_t st) {
     cdist_pairs_kernel<<<blocks, 256, 0, st>>>(first, n, a.row_begin, a.nB, a.lenA, a.lenB, offsets,
                                                lengths);
     ++g_launches;
-    rc = batch_impl(a.A, a.B, offsets, lengths, n, a.dim, a.norm, a.dtype, tmp, ws, wsb, st);
+    rc = batch_impl(a.A, a.B, offsets, lengths, n, a.dim, a.norm, a.dtype, tmp, ws, wsb, st, 0,
+                    pair_goes_long(a.lenA, a.lenB));
     if (rc != FFD_OK) break;
     if (osz == 8)
       cdist_scatter_kernel<long long><<<blocks, 256, 0, st>>>(
@@ -435,9 +438,13 @@ int ffd_batch_host(const void* p_host, int64_t np, const void* q_host, int64_t n
         cudaMemcpyAsync(dlen, lengths_host, lenb, cudaMemcpyHostToDevice, st))
       rc = FFD_ERR_CUDA;
   }
+  bool any_long = false;  // the lengths are on the host: skip the long-pair launch if none is
+  for (int64_t k = 0; k < num_pairs && !any_long; k++)
+    any_long = lengths_host[k] >= 1 && lengths_host[num_pairs + k] >= 1 &&
+               pair_goes_long(lengths_host[k], lengths_host[num_pairs + k]);
   if (rc == FFD_OK)
     rc = batch_impl(dp, dq, reinterpret_cast<int64_t*>(doff), reinterpret_cast<int32_t*>(dlen),
-                    num_pairs, dim, norm, dtype, dout, dws, wsb, st);
+                    num_pairs, dim, norm, dtype, dout, dws, wsb, st, 0, any_long);
   if (rc == FFD_OK && cudaMemcpyAsync(out_host, dout, ob, cudaMemcpyDeviceToHost, st))
     rc = FFD_ERR_CUDA;
   for (void* ptr : {dp, dq, doff, dlen, dout, dws})

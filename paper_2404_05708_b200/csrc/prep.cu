@@ -10,6 +10,43 @@
 
 namespace ffd {
 
+// shape key of pair k, and its descriptor; −1 when the pair is dropped (its
+// invalid-output value written, or sent to the long-pair list)
+__device__ __forceinline__ int pair_key(const int64_t* __restrict__ offsets,
+                                        const int32_t* __restrict__ lengths, int64_t B, int64_t k,
+                                        int int_out, int long_ok, void* __restrict__ out, PairDesc& d,
+                                        int* __restrict__ long_list, int* __restrict__ long_count) {
+  const int n = lengths[k], m = lengths[B + k];
+  if (n < 1 || m < 1) {
+    if (int_out) reinterpret_cast<long long*>(out)[k] = LLONG_MIN;
+    else reinterpret_cast<float*>(out)[k] = __int_as_float(0x7fc00000);
+    return -1;
+  }
+  const bool swap = n > m;
+  const int rows = swap ? m : n, cols = swap ? n : m;
+  const int nb = (rows + kWarp * kMaxR - 1) / (kWarp * kMaxR);
+  if (pair_goes_long(n, m)) {
+    if (long_ok) {
+      long_list[atomicAdd(long_count, 1)] = (int)k;
+    } else {  // no long-pair path for this measure (DTW): documented NaN
+      if (int_out) reinterpret_cast<long long*>(out)[k] = LLONG_MIN;
+      else reinterpret_cast<float*>(out)[k] = __int_as_float(0x7fc00000);
+    }
+    return -1;
+  }
+  const int R = (rows + kWarp * nb - 1) / (kWarp * nb);
+  d.row_off = swap ? offsets[B + k] : offsets[k];
+  d.col_off = swap ? offsets[k] : offsets[B + k];
+  d.n_rows = rows;
+  d.m_cols = cols;
+  d.idx = (int)k;
+  d.R = (uint8_t)R;
+  d.nb = (uint8_t)nb;
+  d.swap = swap;
+  d.pad = 0;
+  return (nb - 1) * kMaxR + (R - 1);
+}
+
 __global__ void prep_keys_kernel(const int64_t* __restrict__ offsets,
                                  const int32_t* __restrict__ lengths, int64_t B, int int_out, int long_ok,
                                  void* __restrict__ out, PairDesc* __restrict__ tmp,
@@ -20,44 +57,74 @@ __global__ void prep_keys_kernel(const int64_t* __restrict__ offsets,
   __syncthreads();
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < B;
        k += (int64_t)gridDim.x * blockDim.x) {
-    const int n = lengths[k], m = lengths[B + k];
-    int key = -1;
-    if (n < 1 || m < 1) {
-      if (int_out) reinterpret_cast<long long*>(out)[k] = LLONG_MIN;
-      else reinterpret_cast<float*>(out)[k] = __int_as_float(0x7fc00000);
-    } else {
-      const bool swap = n > m;
-      const int rows = swap ? m : n, cols = swap ? n : m;
-      const int nb = (rows + kWarp * kMaxR - 1) / (kWarp * kMaxR);
-      if (nb > kMaxBands || (nb > 1 && cols + 2 > kScratchCols)) {
-        if (long_ok) {
-          long_list[atomicAdd(long_count, 1)] = (int)k;
-        } else {  // no long-pair path for this measure (DTW): documented NaN
-          if (int_out) reinterpret_cast<long long*>(out)[k] = LLONG_MIN;
-          else reinterpret_cast<float*>(out)[k] = __int_as_float(0x7fc00000);
-        }
-      } else {
-        const int R = (rows + kWarp * nb - 1) / (kWarp * nb);
-        PairDesc d;
-        d.row_off = swap ? offsets[B + k] : offsets[k];
-        d.col_off = swap ? offsets[k] : offsets[B + k];
-        d.n_rows = rows;
-        d.m_cols = cols;
-        d.idx = (int)k;
-        d.R = (uint8_t)R;
-        d.nb = (uint8_t)nb;
-        d.swap = swap;
-        d.pad = 0;
-        tmp[k] = d;
-        key = (nb - 1) * kMaxR + (R - 1);
-        atomicAdd(&h[key], 1);
-      }
+    PairDesc d;
+    const int key = pair_key(offsets, lengths, B, k, int_out, long_ok, out, d, long_list, long_count);
+    if (key >= 0) {
+      tmp[k] = d;
+      atomicAdd(&h[key], 1);
     }
     keys[k] = (int16_t)key;
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kNumKeys; i += blockDim.x)
     if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+// Small batches (B ≤ kPrepSmallMax): the whole preparation in ONE block of
+// kNumKeys·4 threads — counters zeroed, keys and histogram, the descending scan,
+// the scatter — in place of the memset and three launches of the general path
+// (for config 1's 16 pairs that chain is pure launch latency).  Each thread
+// keeps its pairs' keys and descriptors in registers between the phases.
+constexpr int kPrepSmallThreads = 1024;
+constexpr int kPrepSmallPer = 4;  // pairs per thread
+
+__global__ void __launch_bounds__(kPrepSmallThreads)
+    prep_small_kernel(const int64_t* __restrict__ offsets, const int32_t* __restrict__ lengths,
+                      int64_t B, int int_out, int long_ok, void* __restrict__ out,
+                      int* __restrict__ counters, int* __restrict__ long_list,
+                      PairDesc* __restrict__ sorted) {
+  __shared__ int h[kNumKeys];
+  __shared__ int s[kNumKeys];
+  __shared__ int long_count;
+  for (int i = threadIdx.x; i < kNumKeys; i += blockDim.x) h[i] = 0;
+  if (threadIdx.x == 0) long_count = 0;
+  __syncthreads();
+  PairDesc d[kPrepSmallPer];
+  int key[kPrepSmallPer];
+#pragma unroll
+  for (int u = 0; u < kPrepSmallPer; u++) {
+    const int64_t k = threadIdx.x + (int64_t)u * blockDim.x;
+    key[u] = -1;
+    if (k < B) {
+      key[u] = pair_key(offsets, lengths, B, k, int_out, long_ok, out, d[u], long_list, &long_count);
+      if (key[u] >= 0) atomicAdd(&h[key[u]], 1);
+    }
+  }
+  __syncthreads();
+  // descending exclusive scan over the bins (as prep_scan_kernel)
+  const int i = threadIdx.x;
+  if (i < kNumKeys) s[i] = h[kNumKeys - 1 - i];
+  __syncthreads();
+  for (int o = 1; o < kNumKeys; o <<= 1) {
+    const int v = (i < kNumKeys && i >= o) ? s[i - o] : 0;
+    __syncthreads();
+    if (i < kNumKeys) s[i] += v;
+    __syncthreads();
+  }
+  int total = s[kNumKeys - 1];
+  __syncthreads();
+  if (i < kNumKeys) {
+    const int bin = kNumKeys - 1 - i;
+    h[bin] = s[i] - h[bin];  // h becomes the bin cursors
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kPrepSmallPer; u++)
+    if (key[u] >= 0) sorted[atomicAdd(&h[key[u]], 1)] = d[u];
+  if (threadIdx.x < kNumCtr)
+    counters[threadIdx.x] = threadIdx.x == kCtrNumSorted ? total
+                            : threadIdx.x == kCtrLong    ? long_count
+                                                         : 0;
 }
 
 // one block of kNumKeys threads: descending-key exclusive scan -> bin cursors
@@ -94,6 +161,16 @@ cudaError_t launch_prep(const int64_t* offsets, const int32_t* lengths, int64_t 
                         int long_ok, void* out, const BatchWs& ws, int num_sms, cudaStream_t st,
                         int64_t* launches) {
   if (B == 0) return cudaSuccess;
+  if (B <= kPrepSmallMax) {
+    prep_small_kernel<<<1, kPrepSmallThreads, 0, st>>>(offsets, lengths, B, int_out, long_ok, out,
+                                                       ws.counters, ws.long_list, ws.sorted);
+    *launches += 1;
+    return cudaGetLastError();
+  }
+  if (cudaMemsetAsync(ws.counters, 0,
+                      reinterpret_cast<char*>(ws.cursor) - reinterpret_cast<char*>(ws.counters),
+                      st) != cudaSuccess)
+    return cudaGetLastError();
   const int threads = 256;
   int64_t blocks = (B + threads - 1) / threads;
   if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;

@@ -8,9 +8,20 @@
 
 namespace ffd {
 
-constexpr int kNumKeys = kMaxBands * kMaxR;  // 128 shape bins
+constexpr int kNumKeys = kMaxBands * kMaxR;  // 256 shape bins
+constexpr int64_t kPrepSmallMax = 4096;      // batches up to this size: one-block prep
 
-// counters block (int32 each), zeroed by one memset per call
+// a valid pair (n, m ≥ 1) too long for the batch kernel's bands / band scratch:
+// it goes to the long-pair list (one rule for the device prep and host callers
+// that know the lengths)
+__host__ __device__ inline bool pair_goes_long(int n, int m) {
+  const int rows = n < m ? n : m, cols = n < m ? m : n;
+  const int nb = (rows + kWarp * kMaxR - 1) / (kWarp * kMaxR);
+  return nb > kMaxBands || (nb > 1 && cols + 2 > kScratchCols);
+}
+
+// counters block (int32 each), zeroed per call (by the one-block prep, or a
+// memset of the counters + histogram block)
 enum : int {
   kCtrNumSorted = 0,
   kCtrChunkMain = 1,

@@ -243,3 +243,57 @@ def test_odd_even_columns_and_bands(ffd, norm):
     b = make_batch(rng, len(lens), 0, 0, lens=L)
     out = ffd.batch(*to_dev(b), norm=norm)
     check_float(out.cpu().numpy(), b, norm)
+
+
+@pytest.mark.parametrize("B", [4096, 4097])
+def test_prep_small_and_general_paths_agree(ffd, B):
+    """B ≤ 4096 takes the one-block preparation kernel, larger batches the
+    memset + three-kernel counting sort: both exact against the oracle, with
+    empty and long pairs mixed in (their dropped-pair and long-list paths)."""
+    rng = np.random.default_rng(B)
+    lens = rng.integers(1, 300, size=2 * B).astype(np.int32)
+    lens[5] = 0                       # empty: INT64_MIN
+    lens[B + 7], lens[7] = 9000, 600  # long pair: the long-pair list
+    b = make_batch(rng, B, 1, 300, kind="i", lens=lens)
+    got = ffd.batch(*to_dev(b), norm="sql2").cpu().numpy()
+    ref = oracle.batch(b.p, b.q, b.offsets, b.lengths, b.dim, "sql2", check=False)
+    assert got[5] == np.iinfo(np.int64).min
+    keep = np.arange(B) != 5
+    assert np.array_equal(got[keep], ref[keep])
+
+
+def test_cuda_graph_capture_replay(ffd):
+    """ffd_batch is stream-capturable: one capture, then replays over new data
+    written in place into the same buffers give the oracle's results."""
+    rng = np.random.default_rng(11)
+    b = make_batch(rng, 16, 64, 80)
+    p, q, off, lens = to_dev(b)
+    out = torch.empty(16, dtype=torch.float32, device="cuda")
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        ffd.batch(p, q, off, lens, norm="l2", out=out)   # warm-up outside capture
+    torch.cuda.current_stream().wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        ffd.batch(p, q, off, lens, norm="l2", out=out)
+    for seed in (1, 2, 3):
+        b2 = make_batch(np.random.default_rng(seed), 16, 64, 80, lens=b.lengths)
+        p.copy_(torch.from_numpy(b2.p))
+        q.copy_(torch.from_numpy(b2.q))
+        g.replay()
+        torch.cuda.synchronize()
+        check_float(out.cpu().numpy(), b2, "l2")
+
+
+def test_batch_host_with_and_without_long_pairs(ffd):
+    """ffd_batch_host skips the long-pair launch when its host lengths show no
+    long pair, and runs it when one is there: both exact."""
+    rng = np.random.default_rng(23)
+    for long_pair in (False, True):
+        lens = rng.integers(1, 200, size=2 * 8).astype(np.int32)
+        if long_pair:
+            lens[3], lens[8 + 3] = 700, 9000
+        b = make_batch(rng, 8, 1, 200, kind="i", lens=lens)
+        got = ffd.batch_host(b.p, b.q, b.offsets, b.lengths, norm="l1")
+        assert np.array_equal(got, oracle.batch(b.p, b.q, b.offsets, b.lengths, b.dim, "l1"))

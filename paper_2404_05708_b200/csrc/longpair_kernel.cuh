@@ -294,7 +294,14 @@ struct LongRunner {
     int t = 0, next_refill = 16;
     while (t < total) {
       if (t == next_refill) {
-        if (2 * t < S2) wait_chunk(2 * t + 31, S2, has_in, in, tb);
+        // the slots of this chunk were prefetched one chunk ago: when every tag
+        // is already there, go on without touching the link (a blocking poll of
+        // an L2 link costs ~700 cycles per chunk); else wait on lane 0 first
+        if (2 * t < S2 && has_in) {
+          const int pos = 2 * t + lane;
+          const bool ready = pos >= S2 || pre.y == tb + (unsigned)pos + 1u;
+          if (!__all_sync(0xffffffffu, ready)) wait_chunk(2 * t + 31, S2, has_in, in, tb);
+        }
         store_elem(a, kind, 2 * t + lane, top_of(2 * t + lane, S2, has_in, in, tb, pre), ok);
 #pragma unroll
         for (int cc = 0; cc < D; cc++) a[cc] = a2[cc];
@@ -414,8 +421,24 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
   __syncthreads();
   cl.sync();  // every CTA of the cluster has initialised its rings before any remote access
   const int npairs = *pb.list_count;
-  unsigned tb = 0;  // tag base: absolute stream position of the current pair on every link
+  // CTA groups: several long pairs run side by side, each on a contiguous group
+  // of Gg CTAs (pair li on group li mod NG).  Gg is what the largest pair needs
+  // at R = 16; a single very long pair (config 5) keeps the whole grid.  Every
+  // CTA computes the same NG from the same lengths.
+  int need = 1;
   for (int li = 0; li < npairs; li++) {
+    const int k = pb.list[li];
+    const int n0 = pb.lengths[k], m0 = pb.lengths[pb.num_pairs + k];
+    const int rows = n0 < m0 ? n0 : m0;
+    const int nb16 = (rows + kWarp * 16 - 1) / (kWarp * 16);
+    need = max(need, (nb16 + kLWarps - 1) / kLWarps);
+  }
+  need = min(need, G);
+  const int NG = max(1, min(G / need, npairs));
+  const int Gg = G / NG;
+  const int grp = cta / Gg, local = cta - grp * Gg;
+  unsigned tb = 0;  // tag base: absolute stream position of the current pair on every link
+  for (int li = grp; li < npairs && grp < NG; li += NG) {
     const int k = pb.list[li];
     const int64_t B = pb.num_pairs;
     const int n0 = pb.lengths[k], m0 = pb.lengths[B + k];
@@ -425,10 +448,10 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
                      (swap ? pb.offsets[B + k] : pb.offsets[k]) * D;
     const In* cols = reinterpret_cast<const In*>(swap ? pb.p : pb.q) +
                      (swap ? pb.offsets[k] : pb.offsets[B + k]) * D;
-    const int R = long_rows_per_lane(n, G);
+    const int R = long_rows_per_lane(n, Gg);
     const int S = (m + 2) & ~1;  // stream positions of this pair (even, see run_band)
     if (R == 0) {
-      if (cta == 0 && threadIdx.x == 0) {
+      if (local == 0 && threadIdx.x == 0) {
         if constexpr (INT_IN) reinterpret_cast<long long*>(pb.out)[k] = LLONG_MIN;
         else reinterpret_cast<float*>(pb.out)[k] = __int_as_float(0x7fc00000);
       }
@@ -436,29 +459,31 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
     }
     const int band_rows = kWarp * R;
     const int nb = (n + band_rows - 1) / band_rows;
-    const int b = cta * kLWarps + warp;
-    if (!(b < nb && b > 0) && lane == 0) {
+    const int b = local * kLWarps + warp;  // band of this warp within the group's pair
+    if (!(b < nb && b > 0) && lane == 0 && b > 0) {
       // this warp does not consume its input link for this pair: its producer
       // (if any) writes nothing of it either, so mark the whole stream consumed —
       // otherwise the producer of a later pair would wait on a stale counter
       unsigned* cons = (warp > 0) ? &scons[warp - 1]
-                                  : (crank > 0 ? &scons[kLWarps - 1] : pb.gcons + (cta + G - 1) % G);
+                                  : (crank > 0 ? &scons[kLWarps - 1] : pb.gcons + (cta - 1));
       st_ctr(cons, tb + (unsigned)S);
     }
     if (b < nb) {
       const bool has_in = b > 0, has_out = b + 1 < nb;
       Link in{}, out{};
+      // b > 0 with warp 0 means local > 0: the previous CTA is in this group
       if (warp > 0) {
         in = Link{slink[warp - 1], kLSmemRing - 1u, &scons[warp - 1]};
-      } else if (crank > 0) {  // DSMEM link from the previous CTA of this cluster
+      } else if (b > 0 && crank > 0) {  // DSMEM link from the previous CTA of this cluster
         in = Link{slink[kLWarps - 1], kLSmemRing - 1u, &scons[kLWarps - 1]};
-      } else {
-        const int src = (cta + G - 1) % G;
+      } else if (b > 0) {
+        const int src = cta - 1;
         in = Link{pb.gring + (size_t)src * kLGlobRing, kLGlobRing - 1u, pb.gcons + src};
       }
+      // has_out with warp 7 means the next CTA (local + 1 < Gg) is in this group
       if (warp < kLWarps - 1) {
         out = Link{slink[warp], kLSmemRing - 1u, &scons[warp]};
-      } else if (crank + 1 < csize) {  // DSMEM link into the next CTA of this cluster
+      } else if (has_out && crank + 1 < csize) {  // DSMEM link into the next CTA of this cluster
         out = Link{cl.map_shared_rank(slink[kLWarps - 1], crank + 1), kLSmemRing - 1u,
                    cl.map_shared_rank(&scons[kLWarps - 1], crank + 1)};
       } else {

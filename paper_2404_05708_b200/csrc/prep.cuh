@@ -11,13 +11,25 @@ namespace ffd {
 constexpr int kNumKeys = kMaxBands * kMaxR;  // 256 shape bins
 constexpr int64_t kPrepSmallMax = 4096;      // batches up to this size: one-block prep
 
-// a valid pair (n, m ≥ 1) too long for the batch kernel's bands / band scratch:
-// it goes to the long-pair list (one rule for the device prep and host callers
-// that know the lengths)
-__host__ __device__ inline bool pair_goes_long(int n, int m) {
+// a valid pair (n, m ≥ 1) too long for the batch kernel's bands / band scratch
+__host__ __device__ inline bool pair_too_long(int n, int m) {
   const int rows = n < m ? n : m, cols = n < m ? m : n;
   const int nb = (rows + kWarp * kMaxR - 1) / (kWarp * kMaxR);
   return nb > kMaxBands || (nb > 1 && cols + 2 > kScratchCols);
+}
+
+// Fréchet pairs whose shorter curve needs 8 or more bands of 512 rows run on the
+// long-pair kernel (a group of CTAs per pair, bands pipelined over its warps)
+// instead of one warp walking the bands in sequence: a batch of such pairs
+// rarely has enough of them to fill the GPU one warp each (the paper's E2 sweep:
+// 1024 pairs of 8192 points ran on 1024 warps at 1.9 T cells/s).
+constexpr int kMediumRows = 7 * kWarp * kMaxR;  // 3584
+
+// the rule of the device prep, shared with host callers that know the lengths:
+// the pair goes to the long-pair list
+__host__ __device__ inline bool pair_goes_long(int n, int m) {
+  const int rows = n < m ? n : m;
+  return pair_too_long(n, m) || rows > kMediumRows;
 }
 
 // counters block (int32 each), zeroed per call (by the one-block prep, or a

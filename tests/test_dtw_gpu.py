@@ -87,3 +87,14 @@ def test_dtw_too_long_is_nan(ffd):
     got = run(ffd, p, q, off, lens, "l2")
     assert np.isnan(got[0])
     assert got[1] == oracle.dtw_pair(p[off[1]:off[1] + 40], q[off[3]:off[3] + 50], "l2", mirror=True)
+
+
+def test_dtw_medium_pairs_stay_on_batch_kernel(ffd):
+    """Fréchet sends pairs above 3584 rows to the long-pair kernel; DTW has no
+    long-pair path, so they must stay on the batch kernel's bands (not NaN)."""
+    rng = np.random.default_rng(41)
+    lens = [4000, 3700, 4500, 5000]
+    p, q, off, lens = make(rng, lens)
+    got = run(ffd, p, q, off, lens, "sql2")
+    assert np.isfinite(got).all()
+    check(got, p, q, off, lens, 2, "sql2")

@@ -105,3 +105,50 @@ def test_many_long_pairs_in_one_call(ffd):
     got = run_pairs(ffd, pairs, "l2")
     for k, (p, q) in enumerate(pairs):
         assert got[k] == oracle.pair(p, q, "l2", form="mirror"), k
+
+
+def _check_mirror_batch(got, pairs, norm):
+    P = np.concatenate([p for p, _ in pairs])
+    Q = np.concatenate([q for _, q in pairs])
+    lp = np.array([len(p) for p, _ in pairs], np.int32)
+    lq = np.array([len(q) for _, q in pairs], np.int32)
+    off = np.concatenate([np.concatenate([[0], np.cumsum(lp)[:-1]]),
+                          np.concatenate([[0], np.cumsum(lq)[:-1]])]).astype(np.int64)
+    mir = oracle.batch(P, Q, off, np.concatenate([lp, lq]), P.shape[1], norm, mirror=True)
+    bad = np.flatnonzero(got != mir)
+    assert bad.size == 0, (bad[:5], got[bad[:5]], mir[bad[:5]])
+
+
+@pytest.mark.parametrize("norm", ["l2", "linf"])
+def test_medium_pairs_on_cta_groups(ffd, norm):
+    """Pairs whose shorter curve exceeds 3584 points run on the long-pair kernel,
+    one group of CTAs per pair, several pairs side by side (group = li mod NG)
+    and several pairs in turn on one group; mixed with short pairs."""
+    rng = np.random.default_rng(31)
+    shapes = [(int(rng.integers(3585, 6000)), int(rng.integers(3585, 9000))) for _ in range(40)]
+    shapes += [(int(rng.integers(1, 400)), int(rng.integers(1, 400))) for _ in range(20)]
+    rng.shuffle(shapes)
+    pairs = [(walk(rng, n), walk(rng, m)) for n, m in shapes]
+    _check_mirror_batch(run_pairs(ffd, pairs, norm), pairs, norm)
+
+
+def test_medium_pairs_more_than_groups(ffd):
+    """300 pairs of 3600 points: 148 groups of one CTA, two or three pairs per
+    group in sequence (tag bases advance per group)."""
+    rng = np.random.default_rng(32)
+    pairs = [(walk(rng, 3600, kind="i"), walk(rng, 3600 + k % 7, kind="i")) for k in range(300)]
+    got = run_pairs(ffd, pairs, "sql2")
+    _check_mirror_batch(got, pairs, "sql2")
+
+
+def test_medium_pairs_multi_cta_groups(ffd):
+    """three 8192-point pairs (the paper's E2 top size): groups of many CTAs,
+    cluster DSMEM and L2 links inside each group"""
+    rng = np.random.default_rng(33)
+    pairs = [(walk(rng, 8192), walk(rng, 8192)) for _ in range(3)] + [(walk(rng, 100), walk(rng, 90))]
+    _check_mirror_batch(run_pairs(ffd, pairs, "l1"), pairs, "l1")
+    os.environ["FFD_LONG_CTAS"] = "5"
+    try:
+        _check_mirror_batch(run_pairs(ffd, pairs, "l1"), pairs, "l1")
+    finally:
+        del os.environ["FFD_LONG_CTAS"]

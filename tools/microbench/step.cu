@@ -104,7 +104,6 @@ int main() {
   run<5, 7>("pipe2+st_generic_smem");
   run<6, 7>("pipe2+st_shared");
   run<7, 7>("pipe2+st_global");
-  return 0;
   run<0, 1>("warp_step2");
   run<0, 4>("warp_step2");
   run<0, 8>("warp_step2");

@@ -1,5 +1,6 @@
 // api.cu — the C ABI of include/ffd.h: argument checks, workspace layout,
 // dispatch to the compiled kernel instantiations, stream-ordered launches.
+#include <algorithm>
 #include <atomic>
 #include <climits>
 #include <cstring>
@@ -399,6 +400,18 @@ int ffd_dist_sum(const void* p, const void* q, const int64_t* offsets, const int
                          reinterpret_cast<cudaStream_t>(stream), &g_launches);
 }
 
+// a second stream per device for the host path's uploads (created once)
+static cudaStream_t copy_stream() {
+  static std::mutex mu;
+  static cudaStream_t streams[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> g(mu);
+  if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
+  return streams[dev];
+}
+
 int ffd_batch_host(const void* p_host, int64_t np, const void* q_host, int64_t nq,
                    const int64_t* offsets_host, const int32_t* lengths_host, int64_t num_pairs,
                    int32_t dim, int32_t norm, int32_t dtype, void* out_host, ffd_stream_t stream) {
@@ -418,36 +431,102 @@ int ffd_batch_host(const void* p_host, int64_t np, const void* q_host, int64_t n
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
   });
-  const size_t esz = 4;
-  const size_t pb = (size_t)np * dim * esz, qb = (size_t)nq * dim * esz;
-  const size_t ob = (size_t)num_pairs * (dtype == FFD_I32 ? 8 : 4);
-  const size_t offb = (size_t)num_pairs * 2 * sizeof(int64_t);
-  const size_t lenb = (size_t)num_pairs * 2 * sizeof(int32_t);
-  const size_t wsb = ffd_batch_workspace_bytes(num_pairs);
+  const int64_t B = num_pairs;
+  const size_t esz = 4, ptb = (size_t)dim * esz;  // bytes per point
+  const size_t pb = (size_t)np * ptb, qb = (size_t)nq * ptb;
+  const size_t osz = dtype == FFD_I32 ? 8 : 4;
+  const size_t ob = (size_t)B * osz;
+  const size_t offb = (size_t)B * 2 * sizeof(int64_t);
+  const size_t lenb = (size_t)B * 2 * sizeof(int32_t);
+  const size_t wsb = ffd_batch_workspace_bytes(B);
+  // Pipelined upload: the pairs are cut into K chunks; chunk j starts as soon as
+  // the point prefixes its pairs reach are on the device, while the copy stream
+  // moves the next points (the points dominate the call: 514 MB for config 2).
+  const int K = (pb + qb >= (64u << 20) && B >= 64)
+                    ? (int)std::min<int64_t>(8, std::max<int64_t>(2, (int64_t)((pb + qb) >> 26)))
+                    : 1;
   void *dp = nullptr, *dq = nullptr, *doff = nullptr, *dlen = nullptr, *dout = nullptr, *dws = nullptr;
+  void *coff = nullptr, *clen = nullptr;
   int rc = FFD_OK;
   if (cudaMallocAsync(&dp, pb ? pb : 16, st) || cudaMallocAsync(&dq, qb ? qb : 16, st) ||
       cudaMallocAsync(&doff, offb, st) || cudaMallocAsync(&dlen, lenb, st) ||
-      cudaMallocAsync(&dout, ob, st) || cudaMallocAsync(&dws, wsb, st)) {
+      cudaMallocAsync(&dout, ob, st) || cudaMallocAsync(&dws, wsb, st) ||
+      (K > 1 && (cudaMallocAsync(&coff, offb, st) || cudaMallocAsync(&clen, lenb, st)))) {
     rc = FFD_ERR_CUDA;
   }
-  if (rc == FFD_OK) {
+  if (rc == FFD_OK && K == 1) {
     if (cudaMemcpyAsync(dp, p_host, pb, cudaMemcpyHostToDevice, st) ||
         cudaMemcpyAsync(dq, q_host, qb, cudaMemcpyHostToDevice, st) ||
         cudaMemcpyAsync(doff, offsets_host, offb, cudaMemcpyHostToDevice, st) ||
         cudaMemcpyAsync(dlen, lengths_host, lenb, cudaMemcpyHostToDevice, st))
       rc = FFD_ERR_CUDA;
+    bool any_long = false;  // the lengths are on the host: skip the long-pair launch if none is
+    for (int64_t k = 0; k < B && !any_long; k++)
+      any_long = lengths_host[k] >= 1 && lengths_host[B + k] >= 1 &&
+                 pair_goes_long(lengths_host[k], lengths_host[B + k]);
+    if (rc == FFD_OK)
+      rc = batch_impl(dp, dq, reinterpret_cast<int64_t*>(doff), reinterpret_cast<int32_t*>(dlen), B, dim,
+                      norm, dtype, dout, dws, wsb, st, 0, any_long);
+  } else if (rc == FFD_OK) {
+    cudaStream_t cs = copy_stream();
+    std::vector<cudaEvent_t> ev(K + 1, nullptr);
+    for (auto& e : ev)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming)) rc = FFD_ERR_CUDA;
+    // the allocations above are stream-ordered on `st`: the copy stream waits for them
+    if (rc == FFD_OK && (cudaEventRecord(ev[K], st) || cudaStreamWaitEvent(cs, ev[K], 0) ||
+                         cudaMemcpyAsync(doff, offsets_host, offb, cudaMemcpyHostToDevice, cs) ||
+                         cudaMemcpyAsync(dlen, lengths_host, lenb, cudaMemcpyHostToDevice, cs)))
+      rc = FFD_ERR_CUDA;
+    int64_t have_p = 0, have_q = 0, need_p = 0, need_q = 0;
+    for (int j = 0; j < K && rc == FFD_OK; j++) {
+      const int64_t k0 = B * j / K, k1 = B * (j + 1) / K, bc = k1 - k0;
+      bool any_long = false;
+      for (int64_t k = k0; k < k1; k++) {
+        const int32_t n = lengths_host[k], m = lengths_host[B + k];
+        if (n < 1 || m < 1) continue;
+        need_p = std::max<int64_t>(need_p, offsets_host[k] + n);
+        need_q = std::max<int64_t>(need_q, offsets_host[B + k] + m);
+        any_long = any_long || pair_goes_long(n, m);
+      }
+      need_p = std::min<int64_t>(need_p, np);
+      need_q = std::min<int64_t>(need_q, nq);
+      if (j == K - 1) need_p = np, need_q = nq;  // whatever is left
+      if (need_p > have_p &&
+          cudaMemcpyAsync(static_cast<char*>(dp) + have_p * ptb, static_cast<const char*>(p_host) + have_p * ptb,
+                          (size_t)(need_p - have_p) * ptb, cudaMemcpyHostToDevice, cs))
+        rc = FFD_ERR_CUDA;
+      if (need_q > have_q &&
+          cudaMemcpyAsync(static_cast<char*>(dq) + have_q * ptb, static_cast<const char*>(q_host) + have_q * ptb,
+                          (size_t)(need_q - have_q) * ptb, cudaMemcpyHostToDevice, cs))
+        rc = FFD_ERR_CUDA;
+      have_p = std::max(have_p, need_p);
+      have_q = std::max(have_q, need_q);
+      if (rc != FFD_OK || cudaEventRecord(ev[j], cs) || cudaStreamWaitEvent(st, ev[j], 0)) {
+        rc = FFD_ERR_CUDA;
+        break;
+      }
+      // this chunk's [2·bc] offsets / lengths: two slices of the full arrays
+      int64_t* co = static_cast<int64_t*>(coff) + 2 * k0;
+      int32_t* cl = static_cast<int32_t*>(clen) + 2 * k0;
+      const int64_t* fo = static_cast<const int64_t*>(doff);
+      const int32_t* fl = static_cast<const int32_t*>(dlen);
+      if (cudaMemcpyAsync(co, fo + k0, bc * sizeof(int64_t), cudaMemcpyDeviceToDevice, st) ||
+          cudaMemcpyAsync(co + bc, fo + B + k0, bc * sizeof(int64_t), cudaMemcpyDeviceToDevice, st) ||
+          cudaMemcpyAsync(cl, fl + k0, bc * sizeof(int32_t), cudaMemcpyDeviceToDevice, st) ||
+          cudaMemcpyAsync(cl + bc, fl + B + k0, bc * sizeof(int32_t), cudaMemcpyDeviceToDevice, st)) {
+        rc = FFD_ERR_CUDA;
+        break;
+      }
+      rc = batch_impl(dp, dq, co, cl, bc, dim, norm, dtype, static_cast<char*>(dout) + k0 * osz, dws, wsb,
+                      st, 0, any_long);
+    }
+    if (cudaStreamSynchronize(cs) != cudaSuccess && rc == FFD_OK) rc = FFD_ERR_CUDA;
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
   }
-  bool any_long = false;  // the lengths are on the host: skip the long-pair launch if none is
-  for (int64_t k = 0; k < num_pairs && !any_long; k++)
-    any_long = lengths_host[k] >= 1 && lengths_host[num_pairs + k] >= 1 &&
-               pair_goes_long(lengths_host[k], lengths_host[num_pairs + k]);
-  if (rc == FFD_OK)
-    rc = batch_impl(dp, dq, reinterpret_cast<int64_t*>(doff), reinterpret_cast<int32_t*>(dlen),
-                    num_pairs, dim, norm, dtype, dout, dws, wsb, st, 0, any_long);
   if (rc == FFD_OK && cudaMemcpyAsync(out_host, dout, ob, cudaMemcpyDeviceToHost, st))
     rc = FFD_ERR_CUDA;
-  for (void* ptr : {dp, dq, doff, dlen, dout, dws})
+  for (void* ptr : {dp, dq, doff, dlen, dout, dws, coff, clen})
     if (ptr) cudaFreeAsync(ptr, st);
   if (cudaStreamSynchronize(st) != cudaSuccess && rc == FFD_OK) rc = FFD_ERR_CUDA;
   return rc;

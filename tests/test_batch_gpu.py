@@ -297,3 +297,32 @@ def test_batch_host_with_and_without_long_pairs(ffd):
         b = make_batch(rng, 8, 1, 200, kind="i", lens=lens)
         got = ffd.batch_host(b.p, b.q, b.offsets, b.lengths, norm="l1")
         assert np.array_equal(got, oracle.batch(b.p, b.q, b.offsets, b.lengths, b.dim, "l1"))
+
+
+@pytest.mark.parametrize("layout", ["packed", "shuffled", "one_vs_many"])
+def test_batch_host_pipelined_upload(ffd, layout):
+    """ffd_batch_host with ≥ 64 MB of points cuts the pairs into chunks whose
+    compute overlaps the upload of the next points: exact against the device
+    call for packed, permuted (non-monotone offsets) and one-vs-many layouts."""
+    cfg = workload.CONFIGS[2].scaled(pairs=30000)
+    b = workload.gen_batch(cfg)
+    B = b.num_pairs
+    off, lens = b.offsets.copy(), b.lengths.copy()
+    if layout == "shuffled":
+        perm = np.random.default_rng(1).permutation(B)
+        off = np.concatenate([off[:B][perm], off[B:][perm]])
+        lens = np.concatenate([lens[:B][perm], lens[B:][perm]])
+    elif layout == "one_vs_many":
+        m = int(lens[B])
+        off[B:] = 0
+        lens[B:] = m
+    assert b.p.nbytes + b.q.nbytes >= 64 << 20
+    host = ffd.batch_host(b.p, b.q, off, lens, norm="sql2")
+    d = "cuda"
+    dev = ffd.batch(torch.from_numpy(b.p).to(d), torch.from_numpy(b.q).to(d), torch.from_numpy(off).to(d),
+                    torch.from_numpy(lens).to(d), norm="sql2").cpu().numpy()
+    assert np.array_equal(host, dev)
+    sel = np.random.default_rng(2).choice(B, 300, replace=False)
+    ref = oracle.batch(b.p, b.q, np.concatenate([off[sel], off[B + sel]]),
+                       np.concatenate([lens[sel], lens[B + sel]]), b.dim, "sql2")
+    assert np.array_equal(host[sel], ref)

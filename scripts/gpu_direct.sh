@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_longpair_gpu.py -x -q > gpurun_out/pytest_direct.log 2>&1; echo "pytest rc=$?"; tail -5 gpurun_out/pytest_direct.log
+timeout 600 python bench.py --config 5 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/c5_direct.json 2> gpurun_out/c5_direct.err; echo "c5 rc=$?"; tail -3 gpurun_out/c5_direct.err
+python -c "
+import json; d=json.loads(open('gpurun_out/c5_direct.json').read().splitlines()[-1])
+print(d['value'], d['ms_per_step'], {k:(round(v['kernel_ms'],2), round(v['frac'],3)) for k,v in d['roofline']['per_norm'].items()})"
+timeout 300 python scripts/trace_lags.py 262144

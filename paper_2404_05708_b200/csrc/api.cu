@@ -161,7 +161,8 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
     if (!fb_e) return FFD_ERR_UNSUPPORTED;
   }
 
-  if (launch_prep(offsets, lengths, B, int_in, measure == 0, out, ws, di.sms, st, &g_launches) !=
+  const int long_ok = measure == 0 ? medium_rows_for(B, di.sms) : 0;
+  if (launch_prep(offsets, lengths, B, int_in, long_ok, out, ws, di.sms, st, &g_launches) !=
       cudaSuccess)
     return FFD_ERR_CUDA;
 
@@ -285,7 +286,7 @@ static int cdist_via_batch(const CdistArgs& a, cudaStream_t st) {
                                                lengths);
     ++g_launches;
     rc = batch_impl(a.A, a.B, offsets, lengths, n, a.dim, a.norm, a.dtype, tmp, ws, wsb, st, 0,
-                    pair_goes_long(a.lenA, a.lenB));
+                    pair_goes_long(a.lenA, a.lenB, medium_rows_for(n, dev_info().sms)));
     if (rc != FFD_OK) break;
     if (osz == 8)
       cdist_scatter_kernel<long long><<<blocks, 256, 0, st>>>(
@@ -463,7 +464,7 @@ int ffd_batch_host(const void* p_host, int64_t np, const void* q_host, int64_t n
     bool any_long = false;  // the lengths are on the host: skip the long-pair launch if none is
     for (int64_t k = 0; k < B && !any_long; k++)
       any_long = lengths_host[k] >= 1 && lengths_host[B + k] >= 1 &&
-                 pair_goes_long(lengths_host[k], lengths_host[B + k]);
+                 pair_goes_long(lengths_host[k], lengths_host[B + k], medium_rows_for(B, dev_info().sms));
     if (rc == FFD_OK)
       rc = batch_impl(dp, dq, reinterpret_cast<int64_t*>(doff), reinterpret_cast<int32_t*>(dlen), B, dim,
                       norm, dtype, dout, dws, wsb, st, 0, any_long);
@@ -486,7 +487,7 @@ int ffd_batch_host(const void* p_host, int64_t np, const void* q_host, int64_t n
         if (n < 1 || m < 1) continue;
         need_p = std::max<int64_t>(need_p, offsets_host[k] + n);
         need_q = std::max<int64_t>(need_q, offsets_host[B + k] + m);
-        any_long = any_long || pair_goes_long(n, m);
+        any_long = any_long || pair_goes_long(n, m, medium_rows_for(bc, dev_info().sms));
       }
       need_p = std::min<int64_t>(need_p, np);
       need_q = std::min<int64_t>(need_q, nq);

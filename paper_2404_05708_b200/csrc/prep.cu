@@ -27,7 +27,7 @@ __device__ __forceinline__ int pair_key(const int64_t* __restrict__ offsets,
   const int nb = (rows + kWarp * kMaxR - 1) / (kWarp * kMaxR);
   // DTW (long_ok = 0) has no long-pair path: only the pairs the batch kernel
   // cannot hold leave it (with NaN); Fréchet also sends the medium ones
-  if (long_ok ? pair_goes_long(n, m) : pair_too_long(n, m)) {
+  if (long_ok ? pair_goes_long(n, m, long_ok) : pair_too_long(n, m)) {
     if (long_ok) {
       long_list[atomicAdd(long_count, 1)] = (int)k;
     } else {  // no long-pair path for this measure (DTW): documented NaN

@@ -24,12 +24,18 @@ __host__ __device__ inline bool pair_too_long(int n, int m) {
 // rarely has enough of them to fill the GPU one warp each (the paper's E2 sweep:
 // 1024 pairs of 8192 points ran on 1024 warps at 1.9 T cells/s).
 constexpr int kMediumRows = 7 * kWarp * kMaxR;  // 3584
+// A batch of at most one pair per SM cannot fill the GPU one warp per pair: there
+// every multi-band pair (more than 512 rows) goes to the CTA groups, a CTA or
+// more each (the paper's E1 sweep at N ≤ 128 walks of 1024 points ran on N warps).
+__host__ __device__ inline int medium_rows_for(int64_t num_pairs, int sms) {
+  return num_pairs <= sms ? kWarp * kMaxR : kMediumRows;
+}
 
 // the rule of the device prep, shared with host callers that know the lengths:
-// the pair goes to the long-pair list
-__host__ __device__ inline bool pair_goes_long(int n, int m) {
+// the pair goes to the long-pair list (medium_rows = medium_rows_for(B, SMs))
+__host__ __device__ inline bool pair_goes_long(int n, int m, int medium_rows) {
   const int rows = n < m ? n : m;
-  return pair_too_long(n, m) || rows > kMediumRows;
+  return pair_too_long(n, m) || rows > medium_rows;
 }
 
 // counters block (int32 each), zeroed per call (by the one-block prep, or a
@@ -58,6 +64,8 @@ struct BatchWs {
   size_t bytes;
 };
 
+// long_ok: 0 = no long-pair path (DTW: only pairs too long for the bands leave,
+// with NaN); else the medium-row threshold (medium_rows_for(B, SMs)) of Fréchet
 cudaError_t launch_prep(const int64_t* offsets, const int32_t* lengths, int64_t B, int int_out,
                         int long_ok, void* out, const BatchWs& ws, int num_sms, cudaStream_t st,
                         int64_t* launches);

@@ -40,10 +40,18 @@ def one_vs_many(N, P, Q, seed_first=0):
 def time_gpu(ffd, torch, p, q, off, lens, reps, fn="batch", norm="l2"):
     args = [torch.from_numpy(a).cuda() for a in (p, q, off, lens)]
     call = getattr(ffd, fn)
-    for _ in range(3):
-        call(*args, norm=norm)
-    torch.cuda.synchronize()
+    # the GPU idles (and its clocks drop) while the CPU oracle runs between
+    # points: keep it busy for ≥ 0.3 s before timing, and time ≥ 50 ms of calls
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    call(*args, norm=norm)
+    e1.record()
+    torch.cuda.synchronize()
+    est = max(e0.elapsed_time(e1), 1e-3)
+    for _ in range(max(3, int(300 / est))):
+        call(*args, norm=norm)
+    reps = max(reps, int(50 / est))
+    torch.cuda.synchronize()
     e0.record()
     for _ in range(reps):
         out = call(*args, norm=norm)

@@ -152,3 +152,14 @@ def test_medium_pairs_multi_cta_groups(ffd):
         _check_mirror_batch(run_pairs(ffd, pairs, "l1"), pairs, "l1")
     finally:
         del os.environ["FFD_LONG_CTAS"]
+
+
+def test_small_batch_multiband_pairs_on_groups(ffd):
+    """A batch of at most one pair per SM sends every pair above 512 rows to the
+    CTA groups (E1 at N ≤ 128): exact against the fp32 mirror, with single-band
+    pairs of the same batch staying on the batch kernel."""
+    rng = np.random.default_rng(34)
+    pairs = [(walk(rng, 1024), walk(rng, 1024)) for _ in range(20)]
+    pairs += [(walk(rng, int(rng.integers(513, 3000))), walk(rng, int(rng.integers(513, 3000)))) for _ in range(20)]
+    pairs += [(walk(rng, 300), walk(rng, 2000)), (walk(rng, 40), walk(rng, 30))]
+    _check_mirror_batch(run_pairs(ffd, pairs, "l2"), pairs, "l2")

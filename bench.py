@@ -308,14 +308,17 @@ def bench_ffd(args):
     ffd.profile_enable(True)
     in_bytes = b.p.nbytes + b.q.nbytes + b.offsets.nbytes + b.lengths.nbytes
     flush = in_bytes < L2_FLUSH_BELOW
+    host_ms = None
     with sampler:
         if flush:
             ms = timed_steps_flushed(torch, stream, dev,
                                      lambda: ffd.batch(p, q, off, lens, norm=cfg.norm, out=out), args.steps)
         else:
             e0.record(stream)
+            h0 = time.perf_counter()
             for _ in range(args.steps):
                 ffd.batch(p, q, off, lens, norm=cfg.norm, out=out)
+            host_ms = (time.perf_counter() - h0) * 1e3 / args.steps
             e1.record(stream)
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / args.steps
@@ -418,6 +421,7 @@ def bench_ffd(args):
                 "api": "ffd_batch_host (pinned host buffers, H2D + kernels + D2H per step)"},
         "gpu_launches": launches * args.steps,
         "gpu_launches_per_step": launches,
+        "host_enqueue_ms_per_step": host_ms,
         "checksum": checksum,
     }
     if graph is not None:

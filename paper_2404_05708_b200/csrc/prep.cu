@@ -152,10 +152,20 @@ __global__ void prep_scan_kernel(const int* __restrict__ hist, int* __restrict__
 __global__ void prep_scatter_kernel(const PairDesc* __restrict__ tmp,
                                     const int16_t* __restrict__ keys, int64_t B,
                                     int* __restrict__ cursor, PairDesc* __restrict__ sorted) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < B;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    const int key = keys[k];
-    if (key >= 0) sorted[atomicAdd(&cursor[key], 1)] = tmp[k];
+  // warp-aggregated: the lanes holding the same key take one atomicAdd for all
+  // of them (a batch has only a handful of distinct shapes, so per-pair atomics
+  // on one cursor serialise)
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < B; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = base + threadIdx.x;
+    const int key = k < B ? keys[k] : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const int leader = __ffs(peers) - 1;
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    int pos = 0;
+    if (key >= 0 && lane == leader) pos = atomicAdd(&cursor[key], __popc(peers));
+    pos = __shfl_sync(0xffffffffu, pos, leader);
+    if (key >= 0) sorted[pos + rank] = tmp[k];
   }
 }
 

@@ -530,7 +530,7 @@ def bench_cdist(args):
             "clocks": clocks,
             "cpu_baseline": cpu_baseline_line(args, cfg, ws),
             "roofline": alu_roofline(cells_rank, kern_max, CELL_OF_CONFIG[4], sms, f_max, f_meas,
-                                     "cdist_kernel (fp32 L2, W=8 R=16)", args.traffic),
+                                     "cdist_kernel (fp32 L2, W=4 R=32)", args.traffic),
             "e2e": {"value": total_cells / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": A_h.nbytes + B_h.nbytes,
                     "d2h_bytes_per_step": cfg.nA * cfg.nB * 4},

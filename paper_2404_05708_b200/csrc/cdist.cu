@@ -20,6 +20,9 @@
 //     persistent warps; a rank's shard is a contiguous row range of A.
 #include <climits>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "cdist.cuh"
 #include "ffd.h"
 #include "strip.cuh"
@@ -43,9 +46,10 @@ struct CdistProblem {
 };
 
 constexpr int kCdMinCtasPerSm = 4;  // 128 registers/thread: the W=8, R=16 shape needs ~100
+                                    // (R = 32 shapes: 3 CTAs/SM, 168 registers)
 
 template <int KIND, int D, int W, int R, int FIN>
-__global__ void __launch_bounds__(kWarp* kWarpsPerCta, kCdMinCtasPerSm)
+__global__ void __launch_bounds__(kWarp* kWarpsPerCta, (R > 16) ? 3 : kCdMinCtasPerSm)
     cdist_kernel(const CdistProblem pb) {
   using C = SCfg<float, KIND, D, false>;
   static_assert(!C::XSQ, "cdist: fp32 inputs");
@@ -207,19 +211,22 @@ static cudaError_t launch_one(const CdistProblem& pb, int sms, cudaStream_t st) 
   return cudaGetLastError();
 }
 
-// shapes: (W, R) with W·R ≥ lenA, R ≤ 16; pick the smallest capacity
+// shapes: (W, R) with W·R ≥ lenA; pick the first (smallest capacity) in pick_shape's order
 template <int KIND, int D, int FIN>
 static cudaError_t launch_shape(const CdistProblem& pb, int sms, cudaStream_t st, int W, int R) {
 #define FFD_CD(WW, RR) \
   if (W == WW && R == RR) return launch_one<KIND, D, WW, RR, FIN>(pb, sms, st);
   FFD_CD(8, 4) FFD_CD(8, 8) FFD_CD(8, 16) FFD_CD(16, 12) FFD_CD(16, 16) FFD_CD(32, 12)
-  FFD_CD(32, 16)
+  FFD_CD(32, 16) FFD_CD(4, 32)
 #undef FFD_CD
   return cudaErrorInvalidValue;
 }
 
+// (4, 32) before (8, 16): the same 128 rows with twice the rows per lane halves
+// the per-step shuffle/select/load overhead per cell; at 3 CTAs/SM (168
+// registers) config 4 runs at 5.50 against 5.26 T cells/s
 static void pick_shape(int rows, int& W, int& R) {
-  static const int shapes[][2] = {{8, 4}, {8, 8}, {8, 16}, {16, 12}, {16, 16}, {32, 12}, {32, 16}};
+  static const int shapes[][2] = {{8, 4}, {8, 8}, {4, 32}, {8, 16}, {16, 12}, {16, 16}, {32, 12}, {32, 16}};
   for (auto& sh : shapes)
     if (sh[0] * sh[1] >= rows) {
       W = sh[0];
@@ -237,6 +244,10 @@ int launch_cdist(const CdistArgs& a, int sms, cudaStream_t st, int64_t* launches
   if (a.dim != 2 && a.dim != 3) return FFD_ERR_UNSUPPORTED;
   int W = 0, R = 0;
   pick_shape(a.lenA, W, R);
+  if (const char* env = getenv("FFD_CDIST_SHAPE")) {  // testing: force a built "W,R" shape
+    int w = 0, r = 0;
+    if (sscanf(env, "%d,%d", &w, &r) == 2 && w * r >= a.lenA) W = w, R = r;
+  }
   if (!W) return FFD_ERR_UNSUPPORTED;  // rows longer than one warp band
   if ((int64_t)a.lenB + 1 > INT_MAX / (kCdTile + 1)) return FFD_ERR_UNSUPPORTED;
   CdistProblem pb{};

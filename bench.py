@@ -587,13 +587,13 @@ def bench_long(args):
         ms = timed_steps_flushed(torch, stream, dev, step, args.steps)
     launches = ffd.launches_taken() // args.steps
     # per-norm duration of the dominant (long-pair) kernel: a second, instrumented pass
-    per_norm = {nm: 0.0 for nm in cfg.norms}
+    per_norm = {nm: [] for nm in cfg.norms}
     for _ in range(args.steps):
         for nm in cfg.norms:
             ffd.profile_enable(True)
             ffd.batch(p, q, off, lens, norm=nm, out=outs[nm])
             ffd.profile_enable(False)
-            per_norm[nm] += ffd.profile_take()[0]
+            per_norm[nm].append(ffd.profile_take()[0])
     ffd.launches_taken()
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if ws > 1:
@@ -619,7 +619,9 @@ def bench_long(args):
         f_max = (clocks["sm_max_mhz"] or SM_MAX_MHZ_NOMINAL) * 1e6
         f_meas = (clocks["sm_mhz"] or SM_MAX_MHZ_NOMINAL) * 1e6
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        kern = {nm: per_norm[nm] / args.steps for nm in cfg.norms}
+        # median over the instrumented steps: one slow launch (a cooperative grid
+        # waiting for SMs) must not stand for the kernel
+        kern = {nm: float(np.median(per_norm[nm])) for nm in cfg.norms}
         per = {nm: alu_roofline(cells, kern[nm], CELL_OF_NORM[nm], sms, f_max, f_meas,
                                 f"long_kernel (fp32 {nm})", args.traffic) for nm in cfg.norms}
         line = {

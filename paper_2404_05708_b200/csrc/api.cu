@@ -440,6 +440,8 @@ int ffd_batch_host(const void* p_host, int64_t np, const void* q_host, int64_t n
   const size_t offb = (size_t)B * 2 * sizeof(int64_t);
   const size_t lenb = (size_t)B * 2 * sizeof(int32_t);
   const size_t wsb = ffd_batch_workspace_bytes(B);
+  const int sms = dev_info().sms;
+  const int medium_rows = medium_rows_for(B, sms);
   // Pipelined upload: the pairs are cut into K chunks; chunk j starts as soon as
   // the point prefixes its pairs reach are on the device, while the copy stream
   // moves the next points (the points dominate the call: 514 MB for config 2).
@@ -464,7 +466,7 @@ int ffd_batch_host(const void* p_host, int64_t np, const void* q_host, int64_t n
     bool any_long = false;  // the lengths are on the host: skip the long-pair launch if none is
     for (int64_t k = 0; k < B && !any_long; k++)
       any_long = lengths_host[k] >= 1 && lengths_host[B + k] >= 1 &&
-                 pair_goes_long(lengths_host[k], lengths_host[B + k], medium_rows_for(B, dev_info().sms));
+                 pair_goes_long(lengths_host[k], lengths_host[B + k], medium_rows);
     if (rc == FFD_OK)
       rc = batch_impl(dp, dq, reinterpret_cast<int64_t*>(doff), reinterpret_cast<int32_t*>(dlen), B, dim,
                       norm, dtype, dout, dws, wsb, st, 0, any_long);
@@ -481,13 +483,14 @@ int ffd_batch_host(const void* p_host, int64_t np, const void* q_host, int64_t n
     int64_t have_p = 0, have_q = 0, need_p = 0, need_q = 0;
     for (int j = 0; j < K && rc == FFD_OK; j++) {
       const int64_t k0 = B * j / K, k1 = B * (j + 1) / K, bc = k1 - k0;
+      const int medium_rows_c = medium_rows_for(bc, sms);
       bool any_long = false;
       for (int64_t k = k0; k < k1; k++) {
         const int32_t n = lengths_host[k], m = lengths_host[B + k];
         if (n < 1 || m < 1) continue;
         need_p = std::max<int64_t>(need_p, offsets_host[k] + n);
         need_q = std::max<int64_t>(need_q, offsets_host[B + k] + m);
-        any_long = any_long || pair_goes_long(n, m, medium_rows_for(bc, dev_info().sms));
+        any_long = any_long || pair_goes_long(n, m, medium_rows_c);
       }
       need_p = std::min<int64_t>(need_p, np);
       need_q = std::min<int64_t>(need_q, nq);

@@ -45,9 +45,14 @@ CELL_OF_CONFIG = {1: "f32_d2_sq", 2: "xsq_d2", 3: "f32_d3_sq", 4: "f32_d2_sq", 5
 CELL_OF_NORM = {"l1": "f32_d2_l1", "l2": "f32_d2_sq", "linf": "f32_d2_linf"}
 MIX_SOURCE = "profiles/r1_microbench_pipes_v2.jsonl (tools/microbench/pipes.cu mixcells_*)"
 # dram__bytes_read.sum + dram__bytes_write.sum of one launch of the dominant kernel, from the
-# committed `ncu --set full` capture (profiles/r1_c2_batch_ncu_full_v3.txt: 536.6 MB + 9.4 MB);
-# --traffic overrides.  Algorithmic bytes per launch for c2: 514.3 MB in + 0.8 MB out.
-TRAFFIC_BYTES = {2: 546.0e6}
+# committed ncu captures; --traffic overrides.
+#   c2: profiles/r1_c2_batch_ncu_full_v12.txt, 535.3 MB + 7.2 MB (algorithmic 514.3 MB in + 0.8 MB out)
+#   c3: profiles/r1_traffic_c3.csv, 21.86 GB + 1.60 GB (algorithmic 15.4 GB: the second band of a
+#       pair above 512 rows re-streams its columns and reads the first band's bottom row; at
+#       0.2 TB/s the kernel is nowhere near HBM-bound)
+#   c4: profiles/r1_traffic_c4.csv, 136.3 MB + 1590.8 MB (algorithmic 41 MB in + 1600 MB out)
+#   c5: profiles/r1_traffic_c5.csv (L2 instance), 6.83 MB + 0.02 MB (algorithmic 4.2 MB in)
+TRAFFIC_BYTES = {2: 542.5e6, 3: 23.454e9, 4: 1.7271e9, 5: 6.852e6}
 
 
 L2_FLUSH_BELOW = 256 << 20  # inputs smaller than this could stay in L2 (126 MB) between steps
@@ -530,7 +535,8 @@ def bench_cdist(args):
             "clocks": clocks,
             "cpu_baseline": cpu_baseline_line(args, cfg, ws),
             "roofline": alu_roofline(cells_rank, kern_max, CELL_OF_CONFIG[4], sms, f_max, f_meas,
-                                     "cdist_kernel (fp32 L2, W=4 R=32)", args.traffic),
+                                     "cdist_kernel (fp32 L2, W=4 R=32)",
+                                     args.traffic if args.traffic is not None else TRAFFIC_BYTES.get(4)),
             "e2e": {"value": total_cells / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": A_h.nbytes + B_h.nbytes,
                     "d2h_bytes_per_step": cfg.nA * cfg.nB * 4},
@@ -623,7 +629,9 @@ def bench_long(args):
         # waiting for SMs) must not stand for the kernel
         kern = {nm: float(np.median(per_norm[nm])) for nm in cfg.norms}
         per = {nm: alu_roofline(cells, kern[nm], CELL_OF_NORM[nm], sms, f_max, f_meas,
-                                f"long_kernel (fp32 {nm})", args.traffic) for nm in cfg.norms}
+                                f"long_kernel (fp32 {nm})",
+                                args.traffic if args.traffic is not None
+                                else (TRAFFIC_BYTES.get(5) if nm == "l2" else None)) for nm in cfg.norms}
         line = {
             "metric": METRIC, "value": ws * 3 * cells / (ms_max * 1e-3) / 1e9, "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,

@@ -117,13 +117,19 @@ def _check(status: int, what: str):
 _ws_cache: dict = {}
 
 
-def workspace(nbytes: int, device):
-    """Cached device workspace (grows on demand) per device."""
+def workspace(nbytes: int, device, stream=None):
+    """Cached device workspace (grows on demand), one per (device, stream): calls
+    on different streams run concurrently and must not share scratch.  The
+    buffer is allocated on its stream, so the caching allocator only reuses a
+    replaced buffer in that stream's order."""
     torch = _torch()
-    key = torch.device(device).index
+    dev = torch.device(device)
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    key = (dev.index, s.cuda_stream)
     buf = _ws_cache.get(key)
     if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+        with torch.cuda.stream(s):
+            buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
         _ws_cache[key] = buf
     return buf
 
@@ -162,7 +168,7 @@ def batch(p, q, offsets, lengths, norm="l2", out=None, stream=None, measure="fre
     if out is None:
         out = torch.empty(B, dtype=torch.int64 if dt == I32 else torch.float32, device=p.device)
     ws_bytes = lib().ffd_batch_workspace_bytes(B)
-    ws = workspace(ws_bytes, p.device)
+    ws = workspace(ws_bytes, p.device, stream)
     if measure not in ("frechet", "dtw"):
         raise ValueError(f"unknown measure {measure!r}")
     fn = lib().ffd_batch if measure == "frechet" else lib().ffd_batch_dtw
@@ -226,7 +232,7 @@ def cdist(A, B, norm="l2", rows=None, out=None, ld_out=None, stream=None):
     if out is None:
         out = torch.empty((r1 - r0, ld), dtype=torch.int64 if dt == I32 else torch.float32, device=A.device)
     wsb = lib().ffd_cdist_workspace_bytes()
-    ws = workspace(wsb, A.device) if wsb else None
+    ws = workspace(wsb, A.device, stream) if wsb else None
     _check(lib().ffd_cdist(A.data_ptr(), nA, lenA, B.data_ptr(), nB, lenB, dim, _norm(norm), dt, r0, r1,
                            out.data_ptr(), ld, ws.data_ptr() if ws is not None else None, wsb,
                            _stream_ptr(stream)), "ffd_cdist")
@@ -245,7 +251,7 @@ def cdist_self(A, norm="l2", rows=None, out=None, ld_out=None, stream=None):
     if out is None:
         out = torch.empty((r1 - r0, ld), dtype=torch.int64 if dt == I32 else torch.float32, device=A.device)
     wsb = lib().ffd_cdist_workspace_bytes()
-    ws = workspace(wsb, A.device) if wsb else None
+    ws = workspace(wsb, A.device, stream) if wsb else None
     _check(lib().ffd_cdist_self(A.data_ptr(), nA, lenA, dim, _norm(norm), dt, r0, r1, out.data_ptr(), ld,
                                 ws.data_ptr() if ws is not None else None, wsb, _stream_ptr(stream)),
            "ffd_cdist_self")

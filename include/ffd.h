@@ -109,7 +109,11 @@ int ffd_dist_sum(const void* p, const void* q, const int64_t* offsets, const int
  *   p_host: [np, dim], q_host: [nq, dim]; offsets_host/lengths_host as above;
  *   out_host: float[B] / int64[B].  Host buffers should be pinned for overlap.
  *   Copies in, computes and copies out on `stream` using device memory from a
- *   stream-ordered pool; synchronises `stream` before returning.              */
+ *   stream-ordered pool; synchronises `stream` before returning.  With ≥ 64 MB
+ *   of points the pairs run in up to 8 chunks, each starting as soon as the
+ *   point prefixes its pairs reach have been uploaded by an internal per-device
+ *   copy stream (offsets need not be sorted; unsorted ones just wait longer).
+ *   The host lengths also decide whether the long-pair kernel is launched.     */
 int ffd_batch_host(const void* p_host, int64_t np, const void* q_host, int64_t nq,
                    const int64_t* offsets_host, const int32_t* lengths_host, int64_t num_pairs,
                    int32_t dim, int32_t norm, int32_t dtype, void* out_host, ffd_stream_t stream);

@@ -415,12 +415,20 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   const int csize = (int)cl.num_blocks(), crank = (int)cl.block_rank();
+  const int npairs = *pb.list_count;
   for (int i = threadIdx.x; i < kLWarps * kLSmemRing; i += blockDim.x)
     (&slink[0][0])[i] = make_uint2(0u, 0u);
   if (threadIdx.x < kLWarps) scons[threadIdx.x] = 0u;
+  // this call's global link state: tags restart at 1 every call, so a slot left
+  // from an earlier call must read as empty — zeroed here (instead of a memset
+  // on every batch call, most of which have no long pair) before the grid barrier
+  for (int i = threadIdx.x; i < kLGlobRing; i += blockDim.x)
+    pb.gring[(size_t)cta * kLGlobRing + i] = make_uint2(0u, 0u);
+  if (threadIdx.x == 0) pb.gcons[cta] = 0u;
+  for (int i = cta * (int)blockDim.x + (int)threadIdx.x; i < npairs; i += G * (int)blockDim.x) pb.bad[i] = 0;
   __syncthreads();
   cl.sync();  // every CTA of the cluster has initialised its rings before any remote access
-  const int npairs = *pb.list_count;
+  cg::this_grid().sync();  // and every CTA its global ring before any consumer polls it
   // CTA groups: several long pairs run side by side, each on a contiguous group
   // of Gg CTAs (pair li on group li mod NG).  Gg is what the largest pair needs
   // at R = 16; a single very long pair (config 5) keeps the whole grid.  Every

@@ -22,7 +22,15 @@ __device__ __forceinline__ int pair_key(const int64_t* __restrict__ offsets,
     else reinterpret_cast<float*>(out)[k] = __int_as_float(0x7fc00000);
     return -1;
   }
-  const bool swap = n > m;
+  // Orientation: the rows (held in registers, R per lane) are the shorter curve,
+  // except for Fréchet pairs whose longer curve still fits one band of 32·16
+  // rows: those put the LONGER curve in the rows — fewer column steps, each with
+  // more rows to spread the step's fixed shuffle/select/load cost over.  δ_dF
+  // is symmetric and its value is one of the d_ij, so either orientation gives
+  // the same bits; DTW (long_ok = 0) sums, so it keeps one orientation (the
+  // fp32 mirror's).
+  const bool tall = long_ok && (n > m ? n : m) <= kWarp * kMaxR;
+  const bool swap = tall ? n < m : n > m;
   const int rows = swap ? m : n, cols = swap ? n : m;
   const int nb = (rows + kWarp * kMaxR - 1) / (kWarp * kMaxR);
   // DTW (long_ok = 0) has no long-pair path: only the pairs the batch kernel

@@ -23,13 +23,24 @@ __device__ __forceinline__ int pair_key(const int64_t* __restrict__ offsets,
     return -1;
   }
   // Orientation: the rows (held in registers, R per lane) are the shorter curve,
-  // except for Fréchet pairs whose longer curve still fits one band of 32·16
-  // rows: those put the LONGER curve in the rows — fewer column steps, each with
-  // more rows to spread the step's fixed shuffle/select/load cost over.  δ_dF
+  // unless a Fréchet pair is estimated cheaper with the LONGER curve as rows —
+  // fewer column steps, each with more rows to spread the step's fixed
+  // shuffle/select/load cost over (always so when the longer curve fits one band).  δ_dF
   // is symmetric and its value is one of the d_ij, so either orientation gives
   // the same bits; DTW (long_ok = 0) sums, so it keeps one orientation (the
   // fp32 mirror's).
-  const bool tall = long_ok && (n > m ? n : m) <= kWarp * kMaxR;
+  bool tall = false;
+  if (long_ok) {
+    // estimated issue cost nb · (cols + 32 window steps) · (9.5 + 3.5·R) of each
+    // orientation (the step's fixed part + ~3.5 instructions per cell-row)
+    const int lo = n < m ? n : m, hi = n < m ? m : n;
+    auto cost = [](int r, int c) {
+      const int b = (r + kWarp * kMaxR - 1) / (kWarp * kMaxR);
+      const int rr = (r + kWarp * b - 1) / (kWarp * b);
+      return (float)b * (float)(c + kWarp) * (9.5f + 3.5f * (float)rr);
+    };
+    tall = hi <= kWarp * kMaxR * kMaxBands && cost(hi, lo) < cost(lo, hi);
+  }
   const bool swap = tall ? n < m : n > m;
   const int rows = swap ? m : n, cols = swap ? n : m;
   const int nb = (rows + kWarp * kMaxR - 1) / (kWarp * kMaxR);

@@ -46,13 +46,13 @@ CELL_OF_NORM = {"l1": "f32_d2_l1", "l2": "f32_d2_sq", "linf": "f32_d2_linf"}
 MIX_SOURCE = "profiles/r1_microbench_pipes_v2.jsonl (tools/microbench/pipes.cu mixcells_*)"
 # dram__bytes_read.sum + dram__bytes_write.sum of one launch of the dominant kernel, from the
 # committed ncu captures; --traffic overrides.
-#   c2: profiles/r1_c2_batch_ncu_full_v12.txt, 535.3 MB + 7.2 MB (algorithmic 514.3 MB in + 0.8 MB out)
+#   c2: profiles/r1_c2_batch_ncu_full_v13.txt, 535.8 MB + 6.8 MB (algorithmic 514.3 MB in + 0.8 MB out)
 #   c3: profiles/r1_traffic_c3.csv, 21.86 GB + 1.60 GB (algorithmic 15.4 GB: the second band of a
 #       pair above 512 rows re-streams its columns and reads the first band's bottom row; at
 #       0.2 TB/s the kernel is nowhere near HBM-bound)
 #   c4: profiles/r1_traffic_c4.csv, 136.3 MB + 1590.8 MB (algorithmic 41 MB in + 1600 MB out)
 #   c5: profiles/r1_traffic_c5.csv (L2 instance), 6.83 MB + 0.02 MB (algorithmic 4.2 MB in)
-TRAFFIC_BYTES = {2: 542.5e6, 3: 23.454e9, 4: 1.7271e9, 5: 6.852e6}
+TRAFFIC_BYTES = {2: 542.6e6, 3: 23.454e9, 4: 1.7271e9, 5: 6.852e6}
 
 
 L2_FLUSH_BELOW = 256 << 20  # inputs smaller than this could stay in L2 (126 MB) between steps

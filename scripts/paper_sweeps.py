@@ -20,6 +20,11 @@ import os
 import sys
 import time
 
+# the oracle's OpenMP threads must not spin on every core after each parallel
+# region: they starved the host thread that enqueues the next point's GPU work
+# (two E1/E2 points read 35 % low in r1_paper_sweeps_v5.jsonl)
+os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")
+
 import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

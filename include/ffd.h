@@ -72,7 +72,12 @@ typedef enum {
  *   workspace: device scratch of at least ffd_batch_workspace_bytes(B) bytes,
  *   16-byte aligned, owned by the caller, not read before being written.
  *   Pairs are processed in an order sorted by length; the
- *   result does not depend on that order.
+ *   result does not depend on that order.  Any lengths n, m ≥ 1: a pair too
+ *   long for one warp band is pipelined over groups of CTAs, in as many passes
+ *   as it takes when its bands exceed what the GPU holds at once (linear
+ *   memory, Theorem 1).  Returns FFD_OK once the work is queued; a
+ *   long pair whose pipeline stalls for seconds (a hardware fault, never seen)
+ *   gets NaN / INT64_MIN rather than a plausible value.
  * ------------------------------------------------------------------------- */
 int ffd_batch(const void* p, const void* q, const int64_t* offsets, const int32_t* lengths,
               int64_t num_pairs, int32_t dim, int32_t norm, int32_t dtype, void* out,
@@ -120,6 +125,12 @@ int ffd_batch_host(const void* p_host, int64_t np, const void* q_host, int64_t n
 
 /* ---------------------------------------------------------------------------
  * ffd_cdist — all-pairs distances between two dense curve sets (one shard).
+ *   The paper evaluates δ_dF of a batch of curves against one curve (PAPER
+ *   L259); this is the same pair function (Eq. (1), with lazily
+ *   evaluated d, Theorem 1) over every (A_a, B_b) of two sets — the
+ *   independent pairs the paper parallelises over (L259) — written as a matrix
+ *   block so that W ranks can each compute a block of rows (BASELINE.json
+ *   north_star (3)).
  *   out[(a - row_begin)*ld_out + b] = δ_dF(A_a, B_b)  for a ∈ [row_begin, row_end),
  *   b ∈ [0, nB).  setA: [nA, lenA, dim], setB: [nB, lenB, dim] dense row-major.
  *   out: float (FFD_F32) or int64 (FFD_I32), ld_out ≥ nB elements.

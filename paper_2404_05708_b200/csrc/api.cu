@@ -231,6 +231,10 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
   la.list = ws.long_list;
   la.list_count = ws.counters + kCtrLong;
   la.out = out;
+  // the band scratch of the batch kernel (done with it: stream order) buffers
+  // the wrap link of multi-pass pairs
+  la.wrap = ws.scratch_main;
+  la.wrap_bytes = (size_t)(reinterpret_cast<char*>(ws.scratch_fb) - reinterpret_cast<char*>(ws.scratch_main));
   ProfScope prof(st, 2);
   if (launch_long_pairs(la, di.sms, st, &g_launches) != cudaSuccess) return FFD_ERR_CUDA;
   return FFD_OK;

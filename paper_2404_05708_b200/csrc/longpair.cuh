@@ -14,6 +14,8 @@ struct LongArgs {
   const int* list;        // device list of long pair indices
   const int* list_count;  // device count
   void* out;
+  void* wrap;         // device scratch for the multi-pass wrap link (any contents)
+  size_t wrap_bytes;  // its size
 };
 cudaError_t launch_long_pairs(const LongArgs& a, int sms, cudaStream_t st, int64_t* launches);
 }  // namespace ffd

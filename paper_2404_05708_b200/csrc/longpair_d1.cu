@@ -3,7 +3,8 @@
 #include "longpair_kernel.cuh"
 
 namespace ffd {
-cudaError_t launch_long_dim1(const LongArgs& a, int sms, cudaStream_t st, const LongWs& w, int G) {
-  return launch_long_dim<1>(a, sms, st, w, G);
+cudaError_t launch_long_dim1(const LongArgs& a, int sms, cudaStream_t st, const LongWs& w, int G,
+                             int64_t* launches) {
+  return launch_long_dim<1>(a, sms, st, w, G, launches);
 }
 }  // namespace ffd

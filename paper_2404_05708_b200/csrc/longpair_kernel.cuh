@@ -1,39 +1,59 @@
-// longpair_kernel.cuh — one very long pair spread over the whole GPU
+// longpair_kernel.cuh — very long pairs spread over the whole GPU
 // (BASELINE config 5).
 //
 // What: δ_dF of a pair with n rows (the shorter curve) and m columns, Eq. (1)
 // in linear memory (Theorem 1): every warp keeps only
-// its strip of rows and one column of DP state in registers.
+// its strip of rows and one column of DP state in registers.  Any n and m.
 //
 // How:
 //   * The rows are cut into bands of 32·R rows; band b runs on one warp as the
 //     lane-strip wavefront of strip.cuh (lane ℓ: rows [ℓR, ℓR+R), column t−ℓ at
 //     step t) and streams all m columns once.
 //   * Band b's bottom row (lane 31's value, one per column) is band b+1's top
-//     input.  It moves through LINKS: rings of 8-byte slots {value, tag} written
-//     by lane 31 with one 64-bit store, tag = absolute stream position + 1.  The
-//     consumer polls the slot itself, so data and "ready" arrive together and no
-//     fence or flag is needed (the low-latency protocol NCCL calls LL).  Inside
-//     a CTA the ring is in shared memory; between CTAs (warp 7 → next CTA's
-//     warp 0) it is in global memory (L2).
+//     input.  It moves through LINKS: rings of 8-byte slots {payload, tag}
+//     written by lane 31 (tag = absolute stream position + 1; an int64 value
+//     takes two slots, each with the tag).  The consumer polls the slot itself,
+//     so data and "ready" arrive together and no fence or flag is needed (the
+//     low-latency protocol NCCL calls LL).  Inside a CTA the ring is in shared
+//     memory; between the CTAs of a cluster in the consumer's shared memory
+//     (DSMEM); between clusters in global memory (L2).
 //   * The consumer prefetches the slots of the next 32 columns one chunk ahead
 //     (like the column points), checks the tags when it stores them into its
 //     column ring, and re-polls only the slots that were not ready.  It
 //     publishes how far it has consumed; the producer checks that counter (also
 //     prefetched) before reusing slots: bounded rings, no overwrite.
 //   * Slots are indexed by the ABSOLUTE stream position (tag base + position) so
-//     that slot reuse distance is exactly the ring size across successive pairs —
-//     the flow-control test (consumed + ring > absolute position) is only valid
-//     then.  (Indexing by the position within a pair let a producer that had
-//     moved on to the next pair overwrite the previous pair's last unconsumed
-//     slots whenever a stream length was not a multiple of the ring size: a hang.)
-//   * One persistent CTA of 8 warps per SM, cooperative launch: all bands are
+//     that the slot reuse distance is exactly the ring size across successive
+//     streams — the flow-control test (consumed + capacity > absolute position)
+//     is only valid then.
+//   * Any length (multi-pass): a group of Gg CTAs has NBP = 8·Gg band SLOTS;
+//     band b runs on slot b mod NBP in pass ⌊b / NBP⌋.  The last slot's output
+//     link WRAPS to the first slot, so pass k+1's first band reads pass k's
+//     last band: the passes form one continuous wavefront with no grid barrier.
+//     Slot 0 finishes pass k (a whole stream) before it consumes pass k+1's
+//     input, so the wrap link must buffer one whole stream: it is a ring in HBM
+//     of ≥ S positions (the batch workspace's band scratch, 156 MB on B200:
+//     16M fp32 / 8M int64 positions),
+//     and a multi-pass pair puts its LONGER curve on the rows so that the
+//     buffered stream is the shorter curve (linear memory, Theorem 1).  Every
+//     link carries one stream per pass; the wrap link's stream of pass k+1 is
+//     written in pass k, so its producer tags it with the next pass's base.
+//   * Exact integers: the fp32 tier evaluates int32 input in fp32-exact integer
+//     arithmetic and flags a pair whose points leave the exact
+//     window; the int64 tier (the same kernel with 64-bit state, launched after
+//     it) recomputes exactly the flagged pairs.
+//   * One persistent CTA of 8 warps per SM, cooperative launch: all slots are
 //     co-resident, so spinning on a neighbour cannot deadlock.  Counters and
-//     tags are absolute positions, so successive long pairs need no grid barrier.
+//     tags are absolute positions, so successive passes and pairs need no grid
+//     barrier.
+//   * A spin that sees no progress for ~2.5 s sets a global abort flag (every
+//     other spin then gives up at once) and the pair's result becomes NaN /
+//     INT64_MIN: a hang is never turned into a plausible number.
 #pragma once
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include <cooperative_groups.h>
 
@@ -42,13 +62,13 @@
 
 namespace ffd {
 
-constexpr int kLWarps = 8;          // warps (bands) per CTA
+constexpr int kLWarps = 8;          // warps (band slots) per CTA
 constexpr int kLSmemRing = 1024;    // slots per intra-CTA link (8 KB; the producer may run
                                     // ~500 steps ahead, far beyond the ~47 the consumer needs)
 constexpr int kLGlobRing = 2048;    // slots per inter-CTA link
 constexpr int kMaxLongCtas = 1024;
 // a spin on a link that has not advanced for this many SM cycles (≈ 2.5 s)
-// reports the link state with printf and gives up instead of hanging the GPU
+// reports the link state with printf, sets the abort flag and gives up
 constexpr long long kWatchdogCycles = 5000000000LL;
 
 struct LongProblem {
@@ -60,10 +80,13 @@ struct LongProblem {
   const int* list;
   const int* list_count;
   void* out;
-  uint2* gring;    // [G][kLGlobRing] slots of the link CTA g → g+1 (zeroed per call)
-  unsigned* gcons; // [G] consumer progress on the link CTA g → g+1 (zeroed per call)
-  int* bad;        // per long pair: a point left the fp32-exact window (int input)
-  int trace;       // FFD_LONG_TRACE=1: print each band's start/first-step/end time
+  uint2* gring;    // [G][kLGlobRing] slots of the link CTA g → g+1 (zeroed per launch)
+  unsigned* gcons; // [G + 1] consumer progress on the link CTA g → g+1, [G]: the wrap link
+  uint2* wrap;     // multi-pass wrap link ring (HBM; the batch workspace's band scratch)
+  unsigned wrap_slots;  // its capacity in slots (a power of two)
+  int* bad;        // per long pair: a point left the fp32-exact window (int input, fp32 tier)
+  int* abort;      // a watchdog fired: every spin gives up, results become NaN / INT64_MIN
+  int trace;       // FFD_LONG_TRACE=1: print each band's start/end time
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -77,21 +100,21 @@ __device__ __forceinline__ uint2 ld_slot(const uint2* p) {
   asm volatile("ld.relaxed.gpu.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_slot(uint2* p, float v, unsigned tag) {
-  asm volatile("st.relaxed.gpu.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(__float_as_uint(v)), "r"(tag)
+__device__ __forceinline__ uint4 ld_slot4(const uint2* p) {
+  uint4 v;
+  asm volatile("ld.relaxed.gpu.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
                : "memory");
+  return v;
 }
-__device__ __forceinline__ void st_slot_pred(uint2* p, float v, unsigned tag, int pred) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %3, 0;\n\t@q st.relaxed.gpu.v2.u32 [%0], {%1, %2};\n\t}" ::"l"(p),
-      "r"(__float_as_uint(v)), "r"(tag), "r"(pred)
-      : "memory");
-}
-// two adjacent slots {v0, tag}, {v1, tag + 1} in one predicated 16-byte store
-__device__ __forceinline__ void st_slot2_pred(uint2* p, float v0, float v1, unsigned tag, int pred) {
+// one predicated 16-byte store {a, b, c, d} (no divergent branch per step)
+__device__ __forceinline__ void st_v4_pred(uint2* p, unsigned a, unsigned b, unsigned c, unsigned d,
+                                           int pred) {
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %5, 0;\n\t@q st.relaxed.gpu.v4.u32 [%0], {%1, %2, %3, %4};\n\t}" ::"l"(p),
-      "r"(__float_as_uint(v0)), "r"(tag), "r"(__float_as_uint(v1)), "r"(tag + 1u), "r"(pred));
+      "r"(a), "r"(b), "r"(c), "r"(d), "r"(pred)
+      : "memory");
 }
 __device__ __forceinline__ unsigned ld_ctr(const unsigned* p) {
   unsigned v;
@@ -101,18 +124,65 @@ __device__ __forceinline__ unsigned ld_ctr(const unsigned* p) {
 __device__ __forceinline__ void st_ctr(unsigned* p, unsigned v) {
   asm volatile("st.relaxed.gpu.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ bool aborted(const int* abort) {
+  return *reinterpret_cast<const volatile int*>(abort) != 0;
+}
 
-// one link endpoint: ring of slots (mask = size − 1) and the consumer counter
+// How a DP value of type T moves through {payload, tag} slots.  A = absolute
+// stream position (tag base + position), tag = A + 1.
+template <typename T>
+struct Slots;
+template <>
+struct Slots<float> {  // one slot per position
+  static constexpr unsigned SPP = 1;
+  using Pre = uint2;
+  static __device__ __forceinline__ Pre load(const uint2* ring, unsigned mask, unsigned A) {
+    return ld_slot(ring + (A & mask));
+  }
+  static __device__ __forceinline__ bool ready(const Pre& v, unsigned want) { return v.y == want; }
+  static __device__ __forceinline__ float value(const Pre& v) { return __uint_as_float(v.x); }
+  static __device__ __forceinline__ Pre none() { return make_uint2(0u, 0u); }
+  // positions A (even) and A+1 in one 16-byte store
+  static __device__ __forceinline__ void put2(uint2* ring, unsigned mask, unsigned A, float v0, float v1,
+                                              int pred) {
+    st_v4_pred(ring + (A & mask & ~1u), __float_as_uint(v0), A + 1u, __float_as_uint(v1), A + 2u, pred);
+  }
+};
+template <>
+struct Slots<long long> {  // two slots per position: {lo, tag}, {hi, tag}
+  static constexpr unsigned SPP = 2;
+  using Pre = uint4;
+  static __device__ __forceinline__ Pre load(const uint2* ring, unsigned mask, unsigned A) {
+    return ld_slot4(ring + ((2u * A) & mask));
+  }
+  static __device__ __forceinline__ bool ready(const Pre& v, unsigned want) {
+    return v.y == want && v.w == want;
+  }
+  static __device__ __forceinline__ long long value(const Pre& v) {
+    return (long long)(((unsigned long long)v.z << 32) | v.x);
+  }
+  static __device__ __forceinline__ Pre none() { return make_uint4(0u, 0u, 0u, 0u); }
+  static __device__ __forceinline__ void put2(uint2* ring, unsigned mask, unsigned A, long long v0,
+                                              long long v1, int pred) {
+    uint2* s = ring + ((2u * A) & mask);  // 32-byte aligned: A is even
+    const unsigned long long u0 = (unsigned long long)v0, u1 = (unsigned long long)v1;
+    st_v4_pred(s, (unsigned)u0, A + 1u, (unsigned)(u0 >> 32), A + 1u, pred);
+    st_v4_pred(s + 2, (unsigned)u1, A + 2u, (unsigned)(u1 >> 32), A + 2u, pred);
+  }
+};
+
+// one link endpoint: ring of slots (mask = slots − 1) and the consumer counter
 struct Link {
   uint2* ring;
   unsigned mask;
   unsigned* cons;
 };
 
-template <int KIND, int D, bool INT_IN, int FIN, int R>
+template <typename T, int KIND, int D, bool INT_IN, int FIN, int R>
 struct LongRunner {
-  using T = float;
   using C = SCfg<T, KIND, D, INT_IN>;
+  using SL = Slots<T>;
+  using Pre = typename SL::Pre;
   using In = typename std::conditional<INT_IN, int32_t, float>::type;
   static constexpr int NS = C::NS;
 
@@ -126,35 +196,39 @@ struct LongRunner {
   int n, m;
   int center[D];
 
-  __device__ bool conv(const In (&a)[D], float (&v)[D]) const {
+  // input point → cell coordinates (fp32 tier with int input: translated by the
+  // pair's first row point, false if it leaves the fp32-exact window)
+  __device__ bool conv(const In (&a)[D], T (&v)[D]) const {
     bool ok = true;
 #pragma unroll
     for (int c = 0; c < D; c++) {
-      if constexpr (INT_IN) {
+      if constexpr (INT_IN && C::F) {
         long long t = (long long)a[c] - center[c];
         ok &= (t >= -C::LIM) && (t <= C::LIM);
         v[c] = (float)(int)t;
       } else {
-        v[c] = a[c];
+        v[c] = (T)a[c];
       }
     }
     return ok;
   }
 
   // column element of position `pos` (0 = sentinel), written with its top value
-  __device__ void store_elem(const In (&a)[D], int kind, int pos, float top, bool& ok) {
-    alignas(16) float f[C::EBYTES / 4];
+  __device__ void store_elem(const In (&a)[D], int kind, int pos, T top, bool& ok) {
+    alignas(16) T f[C::EBYTES / sizeof(T)];
 #pragma unroll
-    for (int i = 0; i < C::EBYTES / 4; i++) f[i] = 0.f;
+    for (int i = 0; i < (int)(C::EBYTES / sizeof(T)); i++) f[i] = (T)0;
     if (kind != 0) {
-      if constexpr (C::XSQ) {
+      if constexpr (!C::F) {
+        f[C::I_SENT] = (T)1;
+      } else if constexpr (C::XSQ) {
         f[D] = finf();
       } else {
 #pragma unroll
         for (int c = 0; c < D; c++) f[c] = finf();
       }
     } else {
-      float v[D];
+      T v[D];
       ok &= conv(a, v);
       if constexpr (C::XSQ) {
         int qq = 0;
@@ -195,23 +269,25 @@ struct LongRunner {
 
   // top value of position `pos` for this band: the corner/border for band 0,
   // else the producer's slot (spinning until its tag shows up)
-  __device__ __forceinline__ float top_of(int pos, int S2, bool has_in, const Link& in, unsigned tb,
-                                          uint2 pre) const {
-    if (pos >= S2) return finf();
-    if (!has_in) return pos == 0 ? 0.f : finf();
+  __device__ __forceinline__ T top_of(int pos, int S2, bool has_in, const Link& in, unsigned tb,
+                                      Pre pre) const {
+    if (pos >= S2) return tinf<T>();
+    if (!has_in) return pos == 0 ? (T)0 : tinf<T>();
     const unsigned want = tb + (unsigned)pos + 1u;
-    if (pre.y != want) {
+    if (!SL::ready(pre, want)) {
       const long long t0 = clock64();
-      while (pre.y != want) {
-        pre = ld_slot(in.ring + ((tb + (unsigned)pos) & in.mask));
-        if (clock64() - t0 > kWatchdogCycles) {  // a link that never delivers: report, give up
-          printf("ffd long_kernel watchdog: consumer cta %d lane %d pos %d want tag %u saw %u (tb %u)\n",
-                 (int)blockIdx.x, lane, pos, want, pre.y, tb);
+      while (!SL::ready(pre, want)) {
+        pre = SL::load(in.ring, in.mask, tb + (unsigned)pos);
+        if (aborted(pb.abort)) break;
+        if (clock64() - t0 > kWatchdogCycles) {  // a link that never delivers: report, abort
+          printf("ffd long_kernel watchdog: consumer cta %d lane %d pos %d want tag %u (tb %u)\n",
+                 (int)blockIdx.x, lane, pos, want, tb);
+          atomicExch(pb.abort, 1);
           break;
         }
       }
     }
-    return __uint_as_float(pre.x);
+    return SL::value(pre);
   }
 
   // Wait (lane 0 only, with backoff) until the producer has published position
@@ -224,14 +300,15 @@ struct LongRunner {
     if (has_in && lane == 0) {
       pos = min(pos, S2 - 1);
       const unsigned want = tb + (unsigned)pos + 1u;
-      const uint2* slot = in.ring + ((tb + (unsigned)pos) & in.mask);
-      if (ld_slot(slot).y != want) {
+      if (!SL::ready(SL::load(in.ring, in.mask, tb + (unsigned)pos), want)) {
         const long long t0 = clock64();
-        while (ld_slot(slot).y != want) {
+        while (!SL::ready(SL::load(in.ring, in.mask, tb + (unsigned)pos), want)) {
           __nanosleep(64);
+          if (aborted(pb.abort)) break;
           if (clock64() - t0 > kWatchdogCycles) {
             printf("ffd long_kernel watchdog: chunk wait cta %d pos %d want tag %u (tb %u)\n",
                    (int)blockIdx.x, pos, want, tb);
+            atomicExch(pb.abort, 1);
             break;
           }
         }
@@ -241,20 +318,21 @@ struct LongRunner {
   }
 
   // one band of 32·R rows starting at row r0, two columns per warp step
-  // (strip.cuh warp_step2: lane ℓ at step t works on columns 2(t−ℓ), 2(t−ℓ)+1)
-  __device__ bool run_band(int r0, bool has_in, Link in, bool has_out, Link out, bool last_band,
-                           int out_idx, int* bad_flag, unsigned tb) {
+  // (strip.cuh Pipe2: lane ℓ at step t works on columns 2(t−ℓ), 2(t−ℓ)+1).
+  // tbi / tbo: tag bases of the input / output link streams.
+  __device__ bool run_band(int r0, bool has_in, Link in, unsigned tbi, bool has_out, Link out,
+                           unsigned tbo, bool last_band, int out_idx, int* bad_flag) {
     const int S2 = (m + 2) & ~1;  // positions (even)
     const int NT = S2 / 2;        // steps
     bool ok = true;
-    float x[NS][R], c[R];
+    T x[NS][R], c[R];
 #pragma unroll
     for (int r = 0; r < R; r++) {
       const int row = min(r0 + lane * R + r, n - 1);
       In a[D];
 #pragma unroll
       for (int cc = 0; cc < D; cc++) a[cc] = __ldg(rows + (int64_t)row * D + cc);
-      float v[D];
+      T v[D];
       ok &= conv(a, v);
 #pragma unroll
       for (int cc = 0; cc < D; cc++) x[cc][r] = v[cc];
@@ -264,33 +342,32 @@ struct LongRunner {
         for (int cc = 0; cc < D; cc++) pp += (int)v[cc] * (int)v[cc];
         x[D][r] = (float)pp;
       }
-      c[r] = finf();
+      c[r] = tinf<T>();
     }
-    if constexpr (INT_IN) {
+    if constexpr (INT_IN && C::F) {
       if (!__all_sync(0xffffffffu, ok) && lane == 0) atomicExch(bad_flag, 1);
     }
-    float diag = finf(), b0 = finf();
-    const uint2 none = make_uint2(0u, 0u);
+    T diag = tinf<T>(), b0 = tinf<T>();
     // prologue: positions [0, 32) stored; column points of [32, 64) and [64, 96)
     // in flight (two chunks ahead: one 16-step chunk does not cover the L2/HBM
     // latency of a latency-bound warp); link slots of [32, 64) in flight
     In a[D], a2[D];
     int kind, kind2;
     fetch(lane, S2, a, kind);
-    wait_chunk(31, S2, has_in, in, tb);
-    uint2 pre = (has_in && lane < S2) ? ld_slot(in.ring + ((tb + (unsigned)lane) & in.mask)) : none;
-    store_elem(a, kind, lane, top_of(lane, S2, has_in, in, tb, pre), ok);
+    wait_chunk(31, S2, has_in, in, tbi);
+    Pre pre = (has_in && lane < S2) ? SL::load(in.ring, in.mask, tbi + (unsigned)lane) : SL::none();
+    store_elem(a, kind, lane, top_of(lane, S2, has_in, in, tbi, pre), ok);
     fetch(32 + lane, S2, a, kind);
     fetch(64 + lane, S2, a2, kind2);
-    pre = (has_in && 32 + lane < S2) ? ld_slot(in.ring + ((tb + (unsigned)(32 + lane)) & in.mask)) : none;
+    pre = (has_in && 32 + lane < S2) ? SL::load(in.ring, in.mask, tbi + (unsigned)(32 + lane)) : SL::none();
     __syncwarp();
-    if (has_in && lane == 0) st_ctr(in.cons, tb + (unsigned)min(32, S2));
+    if (has_in && lane == 0) st_ctr(in.cons, tbi + (unsigned)min(32, S2));
+    const unsigned cap = (out.mask + 1u) / SL::SPP;  // output ring capacity in positions
     unsigned cons_seen = 0, cons_next = 0;
     if (has_out) cons_seen = cons_next = ld_ctr(out.cons);
 
     const int total = NT + 31;
     const int pown = (has_out && lane == kWarp - 1) ? 1 : 0;
-    const unsigned omask = out.mask & ~1u;
     int t = 0, next_refill = 16;
     while (t < total) {
       if (t == next_refill) {
@@ -299,33 +376,36 @@ struct LongRunner {
         // an L2 link costs ~700 cycles per chunk); else wait on lane 0 first
         if (2 * t < S2 && has_in) {
           const int pos = 2 * t + lane;
-          const bool ready = pos >= S2 || pre.y == tb + (unsigned)pos + 1u;
-          if (!__all_sync(0xffffffffu, ready)) wait_chunk(2 * t + 31, S2, has_in, in, tb);
+          const bool ready = pos >= S2 || SL::ready(pre, tbi + (unsigned)pos + 1u);
+          if (!__all_sync(0xffffffffu, ready)) wait_chunk(2 * t + 31, S2, has_in, in, tbi);
         }
-        store_elem(a, kind, 2 * t + lane, top_of(2 * t + lane, S2, has_in, in, tb, pre), ok);
+        store_elem(a, kind, 2 * t + lane, top_of(2 * t + lane, S2, has_in, in, tbi, pre), ok);
 #pragma unroll
         for (int cc = 0; cc < D; cc++) a[cc] = a2[cc];
         kind = kind2;
         fetch(2 * t + 64 + lane, S2, a2, kind2);
         const int pn = 2 * t + 32 + lane;
-        pre = (has_in && pn < S2) ? ld_slot(in.ring + ((tb + (unsigned)pn) & in.mask)) : none;
+        pre = (has_in && pn < S2) ? SL::load(in.ring, in.mask, tbi + (unsigned)pn) : SL::none();
         __syncwarp();
-        if (has_in && lane == 0) st_ctr(in.cons, tb + (unsigned)min(2 * t + 32, S2));
+        if (has_in && lane == 0) st_ctr(in.cons, tbi + (unsigned)min(2 * t + 32, S2));
         next_refill += 16;
       }
       if (has_out && (t & 15) == 0) {
-        // lane 31 writes positions < 2t during the next 16 steps: their slots
-        // must be consumed (cons + ring > tb + 2t).  The counter is read a chunk ahead.
+        // lane 31 writes positions < 2t + 32 during the next 16 steps: their
+        // slots must be consumed (cons + capacity > tbo + 2t).  The counter is
+        // read a chunk ahead.
         if (lane == kWarp - 1) {
           cons_seen = cons_next;
-          if ((int)(cons_seen + out.mask + 1u - (tb + 2u * (unsigned)t)) <= 0) {
+          if ((int)(cons_seen + cap - (tbo + 2u * (unsigned)t)) <= 0) {
             const long long t0 = clock64();
-            while ((int)(cons_seen + out.mask + 1u - (tb + 2u * (unsigned)t)) <= 0) {
+            while ((int)(cons_seen + cap - (tbo + 2u * (unsigned)t)) <= 0) {
               __nanosleep(64);
               cons_seen = ld_ctr(out.cons);
+              if (aborted(pb.abort)) break;
               if (clock64() - t0 > kWatchdogCycles) {
-                printf("ffd long_kernel watchdog: producer cta %d warp %d t %d cons %u tb %u ring %u\n",
-                       (int)blockIdx.x, (int)(threadIdx.x >> 5), t, cons_seen, tb, out.mask + 1u);
+                printf("ffd long_kernel watchdog: producer cta %d warp %d t %d cons %u tb %u cap %u\n",
+                       (int)blockIdx.x, (int)(threadIdx.x >> 5), t, cons_seen, tbo, cap);
+                atomicExch(pb.abort, 1);
                 break;
               }
             }
@@ -336,19 +416,17 @@ struct LongRunner {
       __syncwarp();
       const int stop = min(next_refill, total);
       int g = t - lane;
-      // the ring elements of the next step are loaded one step ahead (the
-      // volatile link store would otherwise pin each load next to its use)
       // software-pipelined steps (strip.cuh Pipe2): the distances of step g+1 are
       // computed during step g's chain and the ring element of g+2 is loaded;
       // primed again after every refill (its look-ahead may read unstored slots)
-      Pipe2<float, KIND, D, R, INT_IN> pipe;
+      Pipe2<T, KIND, D, R, INT_IN> pipe;
       pipe.prime(x, ring, g);
       // lane 31 publishes its two bottom-row values {value, tag} of every step
-      // with one predicated 16-byte store (no divergent branch per step)
+      // with one predicated store (no divergent branch per step)
       auto one = [&](int gg) {
         pipe.step(c, diag, b0, x, ring, gg, lane);
-        st_slot2_pred(out.ring + ((tb + 2u * (unsigned)gg) & omask), b0, c[R - 1],
-                      tb + 2u * (unsigned)gg + 1u, pown & ((unsigned)gg < (unsigned)NT));
+        SL::put2(out.ring, out.mask, tbo + 2u * (unsigned)gg, b0, c[R - 1],
+                 pown & ((unsigned)gg < (unsigned)NT));
       };
 #pragma unroll 1
       for (; t + 2 <= stop; t += 2, g += 2) {
@@ -362,37 +440,53 @@ struct LongRunner {
     }
     const bool all_ok = __all_sync(0xffffffffu, ok);
     if (last_band && lane == kWarp - 1) {
+      __threadfence();
+      const bool dead = aborted(pb.abort);
       if constexpr (INT_IN) {
-        __threadfence();
-        const bool bad = !all_ok || *reinterpret_cast<volatile int*>(bad_flag) != 0;
+        bool bad = dead;
+        if constexpr (C::F) bad = bad || !all_ok || *reinterpret_cast<volatile int*>(bad_flag) != 0;
+        // an fp32-tier pair flagged here is recomputed by the int64 tier
         reinterpret_cast<long long*>(pb.out)[out_idx] = bad ? LLONG_MIN : (long long)c[R - 1];
       } else {
         float f = c[R - 1];
         if constexpr (FIN == F_SQRT) f = __fsqrt_rn(f);
-        reinterpret_cast<float*>(pb.out)[out_idx] = f;
+        reinterpret_cast<float*>(pb.out)[out_idx] = dead ? __int_as_float(0x7fc00000) : f;
       }
+    }
+    if constexpr (INT_IN && C::F) {
+      // a column point outside the window (seen by any band): flag for the int64 tier
+      if (!all_ok && lane == 0) atomicExch(bad_flag, 1);
     }
     __syncwarp();
     return all_ok;
   }
 };
 
-// rows per lane for a pair with n rows on G co-resident CTAs: the smallest
-// built R whose bands all fit at once (⌈bands / 8⌉ ≤ G); 0 if none does
-__host__ __device__ inline int long_rows_per_lane(int n, int G) {
-  const int rs[5] = {4, 7, 8, 16, 32};  // the R the long kernel is built for
-  for (int i = 0; i < 5; i++) {
-    const int R = rs[i];
+// Rows per lane for a pair whose rows curve has n points, on a group of G
+// co-resident CTAs: the smallest built R whose bands all fit at once
+// (⌈bands / 8⌉ ≤ G: one pass, returns true); else false and the multi-pass R
+// (R = 32 spills; 16 does not).
+template <typename T>
+__host__ __device__ inline bool long_rows_fit(int n, int G, int& R) {
+  constexpr bool F = std::is_same<T, float>::value;
+  const int rs_f[5] = {4, 7, 8, 16, 32};  // the R the fp32 tier is built for
+  const int rs_i[2] = {4, 8};             // the R the int64 tier is built for
+  const int* rs = F ? rs_f : rs_i;
+  const int nr = F ? 5 : 2;
+  for (int i = 0; i < nr; i++) {
+    R = rs[i];
     const int nb = (n + kWarp * R - 1) / (kWarp * R);
-    if ((nb + kLWarps - 1) / kLWarps <= G) return R;
+    if ((nb + kLWarps - 1) / kLWarps <= G) return true;
   }
-  return 0;
+  R = F ? 16 : 8;
+  return false;
 }
 
-template <int KIND, int D, bool INT_IN, int FIN>
+template <typename T, int KIND, int D, bool INT_IN, int FIN>
 __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProblem pb) {
-  using C = SCfg<float, KIND, D, INT_IN>;
+  using C = SCfg<T, KIND, D, INT_IN>;
   using In = typename std::conditional<INT_IN, int32_t, float>::type;
+  constexpr bool TIER64 = !C::F;  // int64 tier: only the pairs the fp32 tier flagged
   // dynamic shared memory: [kLWarps][kLSmemRing] link slots, [kLWarps][kRing·EW]
   // column rings, [kLWarps] consumer counters
   extern __shared__ uint4 lsm[];
@@ -402,63 +496,136 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
   unsigned* scons = reinterpret_cast<unsigned*>(lsm + kLWarps * kLSmemRing / 2 + kLWarps * kRing * C::EW);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x, cta = blockIdx.x;
+  const int npairs = *pb.list_count;
+  // the pairs this launch computes: all long pairs (fp32 tier), or the flagged
+  // ones (int64 tier); every CTA derives the same selection
+  auto selected = [&](int li) { return !TIER64 || pb.bad[li] != 0; };
+  int nsel = 0;
+  for (int li = 0; li < npairs; li++) nsel += selected(li) ? 1 : 0;
+  // nothing to do (the common case of a batch without long pairs): leave before
+  // initialising 64 KB of link rings; every CTA takes the same exit, so no
+  // cluster barrier is left waiting
+  if (nsel == 0) return;
   // Thread-block cluster: consecutive CTAs of a cluster link warp 7 → next CTA's
   // warp 0 through DISTRIBUTED shared memory (the producer stores {value, tag}
   // slots straight into the consumer CTA's smem ring slink[7], which warp 7 of
   // that CTA does not use itself; the consumer publishes its progress into its
-  // own scons[7], which the producer reads remotely).  Only the link between
-  // clusters goes through L2.
-  // nothing to do (the common case of a batch without long pairs): leave before
-  // initialising 64 KB of link rings; every CTA takes the same exit, so no
-  // cluster barrier is left waiting
-  if (*pb.list_count == 0) return;
+  // own scons[7], which the producer reads remotely).  Links between clusters,
+  // and the wrap link of a group, go through L2.
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   const int csize = (int)cl.num_blocks(), crank = (int)cl.block_rank();
-  const int npairs = *pb.list_count;
   for (int i = threadIdx.x; i < kLWarps * kLSmemRing; i += blockDim.x)
     (&slink[0][0])[i] = make_uint2(0u, 0u);
   if (threadIdx.x < kLWarps) scons[threadIdx.x] = 0u;
-  // this call's global link state: tags restart at 1 every call, so a slot left
-  // from an earlier call must read as empty — zeroed here (instead of a memset
-  // on every batch call, most of which have no long pair) before the grid barrier
+  // this launch's global link state: tags restart at 1 every launch, so a slot
+  // left from an earlier launch must read as empty — zeroed here (instead of a
+  // memset on every batch call, most of which have no long pair) before the
+  // grid barrier
   for (int i = threadIdx.x; i < kLGlobRing; i += blockDim.x)
     pb.gring[(size_t)cta * kLGlobRing + i] = make_uint2(0u, 0u);
   if (threadIdx.x == 0) pb.gcons[cta] = 0u;
-  for (int i = cta * (int)blockDim.x + (int)threadIdx.x; i < npairs; i += G * (int)blockDim.x) pb.bad[i] = 0;
+  if constexpr (!TIER64) {
+    for (int i = cta * (int)blockDim.x + (int)threadIdx.x; i < npairs; i += G * (int)blockDim.x) pb.bad[i] = 0;
+    if (cta == 0 && threadIdx.x == 0) *pb.abort = 0;
+  }
   __syncthreads();
   cl.sync();  // every CTA of the cluster has initialised its rings before any remote access
   cg::this_grid().sync();  // and every CTA its global ring before any consumer polls it
   // CTA groups: several long pairs run side by side, each on a contiguous group
-  // of Gg CTAs (pair li on group li mod NG).  Gg is what the largest pair needs
-  // at R = 16; a single very long pair (config 5) keeps the whole grid.  Every
-  // CTA computes the same NG from the same lengths.
+  // of Gg CTAs (selected pair lj on group lj mod NG).  Gg is what the largest
+  // pair needs at R = 16 (int64 tier: 8); a single very long pair (config 5) keeps the whole
+  // grid.  Every CTA computes the same NG from the same lengths.
   int need = 1;
   for (int li = 0; li < npairs; li++) {
+    if (!selected(li)) continue;
     const int k = pb.list[li];
     const int n0 = pb.lengths[k], m0 = pb.lengths[pb.num_pairs + k];
     const int rows = n0 < m0 ? n0 : m0;
-    const int nb16 = (rows + kWarp * 16 - 1) / (kWarp * 16);
-    need = max(need, (nb16 + kLWarps - 1) / kLWarps);
+    constexpr int RN = C::F ? 16 : 8;  // the tallest band without spills
+    const int nbn = (rows + kWarp * RN - 1) / (kWarp * RN);
+    need = max(need, (nbn + kLWarps - 1) / kLWarps);
   }
   need = min(need, G);
-  const int NG = max(1, min(G / need, npairs));
+  const int NG = max(1, min(G / need, nsel));
   const int Gg = G / NG;
+  // Multi-pass pairs (only possible with one group: every pair fits one pass on
+  // a group of `need` CTAs) stream their SHORTER curve as columns through the
+  // HBM wrap link, whose ring is sized once per launch to the longest such
+  // stream (wrap_mask + 1 slots) and zeroed here: tags restart every launch.
+  unsigned wrap_mask = 0;
+  for (int li = 0; li < npairs && NG == 1; li++) {
+    if (!selected(li)) continue;
+    const int k = pb.list[li];
+    const int n0 = pb.lengths[k], m0 = pb.lengths[pb.num_pairs + k];
+    int Rx;
+    if (long_rows_fit<T>(n0 < m0 ? n0 : m0, Gg, Rx)) continue;
+    const unsigned long long need_slots =
+        (unsigned long long)((min(n0, m0) + 2) & ~1) * Slots<T>::SPP;
+    unsigned long long cap = 2;
+    while (cap < need_slots) cap <<= 1;
+    if (cap <= pb.wrap_slots) wrap_mask = max(wrap_mask, (unsigned)(cap - 1ull));
+  }
+  if (wrap_mask)
+    for (size_t i = (size_t)cta * blockDim.x + threadIdx.x; i <= (size_t)wrap_mask; i += (size_t)G * blockDim.x)
+      pb.wrap[i] = make_uint2(0u, 0u);
+  if (cta == 0 && threadIdx.x == 0) pb.gcons[G] = 0u;
+  if constexpr (!TIER64) {
+    for (int i = cta * (int)blockDim.x + (int)threadIdx.x; i < npairs; i += G * (int)blockDim.x) pb.bad[i] = 0;
+    if (cta == 0 && threadIdx.x == 0) *pb.abort = 0;
+  }
+  __syncthreads();
+  cl.sync();  // every CTA of the cluster has initialised its rings before any remote access
+  cg::this_grid().sync();  // and every CTA its global ring before any consumer polls it
   const int grp = cta / Gg, local = cta - grp * Gg;
-  unsigned tb = 0;  // tag base: absolute stream position of the current pair on every link
-  for (int li = grp; li < npairs && grp < NG; li += NG) {
+  const int last = grp * Gg + Gg - 1;    // the group's last CTA
+  const int NBP = Gg * kLWarps;          // band slots of the group
+  const int j = local * kLWarps + warp;  // this warp's slot
+  const Link wrapL{pb.wrap, wrap_mask, pb.gcons + G};  // multi-pass: last slot → slot 0
+  // the links of this slot (fixed for the launch): input from slot j − 1 (slot
+  // 0: the wrap link from the group's last slot), output to slot j + 1 (the last
+  // slot: the wrap link)
+  Link in{}, out{};
+  if (warp > 0) {
+    in = Link{slink[warp - 1], kLSmemRing - 1u, &scons[warp - 1]};
+  } else if (local > 0 && crank > 0) {  // DSMEM link from the previous CTA of this cluster
+    in = Link{slink[kLWarps - 1], kLSmemRing - 1u, &scons[kLWarps - 1]};
+  } else {  // L2 link from the previous CTA of the group (local 0: the wrap link)
+    const int src = local > 0 ? cta - 1 : last;
+    in = Link{pb.gring + (size_t)src * kLGlobRing, kLGlobRing - 1u, pb.gcons + src};
+  }
+  if (warp < kLWarps - 1) {
+    out = Link{slink[warp], kLSmemRing - 1u, &scons[warp]};
+  } else if (local + 1 < Gg && crank + 1 < csize) {  // DSMEM link into the next CTA of this cluster
+    out = Link{cl.map_shared_rank(slink[kLWarps - 1], crank + 1), kLSmemRing - 1u,
+               cl.map_shared_rank(&scons[kLWarps - 1], crank + 1)};
+  } else {
+    out = Link{pb.gring + (size_t)cta * kLGlobRing, kLGlobRing - 1u, pb.gcons + cta};
+  }
+  unsigned tb = 0;  // tag base: absolute stream position of the current pass on every link
+  int li = -1, lsel = -1;  // li: list index of the lsel-th selected pair
+  for (int lj = grp; lj < nsel && grp < NG; lj += NG) {
+    while (lsel < lj) {
+      ++li;
+      if (selected(li)) ++lsel;
+    }
     const int k = pb.list[li];
     const int64_t B = pb.num_pairs;
     const int n0 = pb.lengths[k], m0 = pb.lengths[B + k];
-    const bool swap = n0 > m0;
+    int R;
+    // one pass: the shorter curve on the rows; multi-pass: the longer one (the
+    // wrap link then buffers the shorter curve's stream)
+    const bool multi = !long_rows_fit<T>(n0 < m0 ? n0 : m0, Gg, R);
+    const bool swap = multi ? n0 < m0 : n0 > m0;
     const int n = swap ? m0 : n0, m = swap ? n0 : m0;
     const In* rows = reinterpret_cast<const In*>(swap ? pb.q : pb.p) +
                      (swap ? pb.offsets[B + k] : pb.offsets[k]) * D;
     const In* cols = reinterpret_cast<const In*>(swap ? pb.p : pb.q) +
                      (swap ? pb.offsets[k] : pb.offsets[B + k]) * D;
-    const int R = long_rows_per_lane(n, Gg);
-    const int S = (m + 2) & ~1;  // stream positions of this pair (even, see run_band)
-    if (R == 0) {
+    const unsigned S = (unsigned)((m + 2) & ~1);  // stream positions of this pair (even, see run_band)
+    if (multi && (unsigned long long)S * Slots<T>::SPP > (unsigned long long)wrap_mask + 1ull) {
+      // the wrap ring cannot buffer this stream (both curves longer than the
+      // band scratch holds: > 16M points, int64 tier 8M): documented limit, no plausible value
       if (local == 0 && threadIdx.x == 0) {
         if constexpr (INT_IN) reinterpret_cast<long long*>(pb.out)[k] = LLONG_MIN;
         else reinterpret_cast<float*>(pb.out)[k] = __int_as_float(0x7fc00000);
@@ -467,69 +634,66 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
     }
     const int band_rows = kWarp * R;
     const int nb = (n + band_rows - 1) / band_rows;
-    const int b = local * kLWarps + warp;  // band of this warp within the group's pair
-    if (!(b < nb && b > 0) && lane == 0 && b > 0) {
-      // this warp does not consume its input link for this pair: its producer
-      // (if any) writes nothing of it either, so mark the whole stream consumed —
-      // otherwise the producer of a later pair would wait on a stale counter
-      unsigned* cons = (warp > 0) ? &scons[warp - 1]
-                                  : (crank > 0 ? &scons[kLWarps - 1] : pb.gcons + (cta - 1));
-      st_ctr(cons, tb + (unsigned)S);
-    }
-    if (b < nb) {
-      const bool has_in = b > 0, has_out = b + 1 < nb;
-      Link in{}, out{};
-      // b > 0 with warp 0 means local > 0: the previous CTA is in this group
-      if (warp > 0) {
-        in = Link{slink[warp - 1], kLSmemRing - 1u, &scons[warp - 1]};
-      } else if (b > 0 && crank > 0) {  // DSMEM link from the previous CTA of this cluster
-        in = Link{slink[kLWarps - 1], kLSmemRing - 1u, &scons[kLWarps - 1]};
-      } else if (b > 0) {
-        const int src = cta - 1;
-        in = Link{pb.gring + (size_t)src * kLGlobRing, kLGlobRing - 1u, pb.gcons + src};
+    const int passes = (nb + NBP - 1) / NBP;
+    const Link lin = (multi && j == 0) ? wrapL : in;
+    const Link lout = (multi && j == NBP - 1) ? wrapL : out;
+    for (int pass = 0; pass < passes; pass++) {
+      const int b = pass * NBP + j;  // band of this slot in this pass
+      if (!(b < nb && b > 0) && lane == 0) {
+        // this slot does not consume its input link in this pass: nobody writes
+        // that stream either, so mark it consumed — otherwise the producer of a
+        // later stream would wait on a stale counter
+        st_ctr(lin.cons, tb + S);
       }
-      // has_out with warp 7 means the next CTA (local + 1 < Gg) is in this group
-      if (warp < kLWarps - 1) {
-        out = Link{slink[warp], kLSmemRing - 1u, &scons[warp]};
-      } else if (has_out && crank + 1 < csize) {  // DSMEM link into the next CTA of this cluster
-        out = Link{cl.map_shared_rank(slink[kLWarps - 1], crank + 1), kLSmemRing - 1u,
-                   cl.map_shared_rank(&scons[kLWarps - 1], crank + 1)};
-      } else {
-        out = Link{pb.gring + (size_t)cta * kLGlobRing, kLGlobRing - 1u, pb.gcons + cta};
-      }
-      auto go = [&](auto& run) {
-        run.n = n;
-        run.m = m;
-        run.rows = rows;
-        run.cols = cols;
-        if constexpr (INT_IN) {
+      if (b < nb) {
+        const bool has_in = b > 0, has_out = b + 1 < nb;
+        // the wrap link's stream belongs to the next pass (its consumer, slot 0, reads it then)
+        const unsigned tbo = (j == NBP - 1) ? tb + S : tb;
+        auto go = [&](auto& run) {
+          run.n = n;
+          run.m = m;
+          run.rows = rows;
+          run.cols = cols;
+          if constexpr (INT_IN) {
 #pragma unroll
-          for (int c = 0; c < D; c++) run.center[c] = (int)rows[c];
+            for (int c = 0; c < D; c++) run.center[c] = (int)rows[c];
+          }
+          const unsigned long long t0 = pb.trace ? gtimer() : 0ull;
+          run.run_band(b * band_rows, has_in, lin, tb, has_out, lout, tbo, b == nb - 1, k, pb.bad + li);
+          if (pb.trace && lane == 0)
+            printf("ffdtrace band %d cta %d warp %d start %llu end %llu\n", b, cta, warp, t0, gtimer());
+        };
+        if constexpr (TIER64) {
+          if (R == 4) {
+            LongRunner<T, KIND, D, INT_IN, FIN, 4> run{rings[warp], pb, lane};
+            go(run);
+          } else {
+            LongRunner<T, KIND, D, INT_IN, FIN, 8> run{rings[warp], pb, lane};
+            go(run);
+          }
+        } else {
+          if (R == 4) {
+            LongRunner<T, KIND, D, INT_IN, FIN, 4> run{rings[warp], pb, lane};
+            go(run);
+          } else if (R == 7) {
+            LongRunner<T, KIND, D, INT_IN, FIN, 7> run{rings[warp], pb, lane};
+            go(run);
+          } else if (R == 8) {
+            LongRunner<T, KIND, D, INT_IN, FIN, 8> run{rings[warp], pb, lane};
+            go(run);
+          } else if (R == 16) {
+            LongRunner<T, KIND, D, INT_IN, FIN, 16> run{rings[warp], pb, lane};
+            go(run);
+          } else {
+            LongRunner<T, KIND, D, INT_IN, FIN, 32> run{rings[warp], pb, lane};
+            go(run);
+          }
         }
-        const unsigned long long t0 = pb.trace ? gtimer() : 0ull;
-        run.run_band(b * band_rows, has_in, in, has_out, out, b == nb - 1, k, pb.bad + li, tb);
-        if (pb.trace && lane == 0)
-          printf("ffdtrace band %d cta %d warp %d start %llu end %llu\n", b, cta, warp, t0, gtimer());
-      };
-      if (R == 4) {
-        LongRunner<KIND, D, INT_IN, FIN, 4> run{rings[warp], pb, lane};
-        go(run);
-      } else if (R == 7) {
-        LongRunner<KIND, D, INT_IN, FIN, 7> run{rings[warp], pb, lane};
-        go(run);
-      } else if (R == 8) {
-        LongRunner<KIND, D, INT_IN, FIN, 8> run{rings[warp], pb, lane};
-        go(run);
-      } else if (R == 16) {
-        LongRunner<KIND, D, INT_IN, FIN, 16> run{rings[warp], pb, lane};
-        go(run);
-      } else {
-        LongRunner<KIND, D, INT_IN, FIN, 32> run{rings[warp], pb, lane};
-        go(run);
       }
+      __syncwarp();
+      tb += S;  // every link's absolute position advances by one stream per pass
     }
     __syncthreads();
-    tb += (unsigned)S;  // every link's absolute position advances by one stream per pair
   }
   cl.sync();  // no CTA leaves while a cluster neighbour may still access its smem
 }
@@ -538,14 +702,15 @@ struct LongWs {
   uint2* gring;
   unsigned* gcons;
   int* bad;
+  int* abort;
 };
 
-// One persistent CTA (8 bands) per SM, cooperative launch.  BASELINE config 5
-// (n = 262,144) runs as 147 CTAs of 8 bands × 224 rows (R = 7).
-template <int KIND, int D, bool INT_IN, int FIN>
+// One persistent CTA (8 band slots) per SM, cooperative launch.  BASELINE
+// config 5 (n = 262,144) runs as 147 CTAs of 8 bands × 224 rows (R = 7).
+template <typename T, int KIND, int D, bool INT_IN, int FIN>
 cudaError_t launch_long_k(const LongArgs& a, int sms, cudaStream_t st, const LongWs& w, int G) {
-  auto k = long_kernel<KIND, D, INT_IN, FIN>;
-  using C = SCfg<float, KIND, D, INT_IN>;
+  auto k = long_kernel<T, KIND, D, INT_IN, FIN>;
+  using C = SCfg<T, KIND, D, INT_IN>;
   const size_t smem = sizeof(uint2) * kLWarps * kLSmemRing + sizeof(uint4) * kLWarps * kRing * C::EW +
                       sizeof(unsigned) * kLWarps;
   // per-device caches: attribute, occupancy and the cluster shape for this grid
@@ -563,12 +728,12 @@ cudaError_t launch_long_k(const LongArgs& a, int sms, cudaStream_t st, const Lon
   if (occ < 1) return cudaErrorLaunchOutOfResources;
   if (G > sms * occ) G = sms * occ;
   static const int trace = getenv("FFD_LONG_TRACE") ? atoi(getenv("FFD_LONG_TRACE")) : 0;
-  LongProblem pb{a.p,      a.q,       a.offsets, a.lengths, a.num_pairs, a.list,
-                 a.list_count, a.out, w.gring,   w.gcons,   w.bad, trace};
+  unsigned wrap_slots = 0;  // the largest power of two of slots the wrap buffer holds
+  for (unsigned long long c = 1; c * sizeof(uint2) <= a.wrap_bytes && c <= 0x80000000ull; c <<= 1)
+    wrap_slots = (unsigned)c;
+  LongProblem pb{a.p,     a.q,     a.offsets, a.lengths,  a.num_pairs, a.list, a.list_count, a.out,
+                 w.gring, w.gcons, reinterpret_cast<uint2*>(a.wrap), wrap_slots, w.bad, w.abort, trace};
   void* args[] = {&pb};
-  // clusters of 8 CTAs (DSMEM links inside a cluster), cooperative so that every
-  // CTA is co-resident; falls back to plain cooperative CTAs if the device
-  // cannot co-schedule the clusters (FFD_LONG_CLUSTER=1 forces that)
   // cluster size: the largest of 8/4/2 whose clusters can all be co-resident
   // for the whole grid (a smaller grid forces taller bands); FFD_LONG_CLUSTER=c
   // forces c (1: none).
@@ -604,7 +769,6 @@ cudaError_t launch_long_k(const LongArgs& a, int sms, cudaStream_t st, const Lon
     }
     const int g = (nclusters < G / csz ? nclusters : G / csz) * csz;
     // only a shape that keeps the whole grid: fewer CTAs would force taller bands
-    // (or leave a pair that needs every CTA without a feasible R)
     if (g == G) {
       best_g = g;
       best_c = csz;
@@ -627,23 +791,32 @@ cudaError_t launch_long_k(const LongArgs& a, int sms, cudaStream_t st, const Lon
 }
 
 // per-dimension dispatch (longpair_d<D>.cu)
-cudaError_t launch_long_dim1(const LongArgs& a, int sms, cudaStream_t st, const LongWs& w, int G);
-cudaError_t launch_long_dim2(const LongArgs& a, int sms, cudaStream_t st, const LongWs& w, int G);
-cudaError_t launch_long_dim3(const LongArgs& a, int sms, cudaStream_t st, const LongWs& w, int G);
-cudaError_t launch_long_dim4(const LongArgs& a, int sms, cudaStream_t st, const LongWs& w, int G);
+cudaError_t launch_long_dim1(const LongArgs& a, int sms, cudaStream_t st, const LongWs& w, int G, int64_t* n);
+cudaError_t launch_long_dim2(const LongArgs& a, int sms, cudaStream_t st, const LongWs& w, int G, int64_t* n);
+cudaError_t launch_long_dim3(const LongArgs& a, int sms, cudaStream_t st, const LongWs& w, int G, int64_t* n);
+cudaError_t launch_long_dim4(const LongArgs& a, int sms, cudaStream_t st, const LongWs& w, int G, int64_t* n);
 
+// fp32 input: one launch.  int32 input: the fp32-exact tier, then the exact
+// int64 tier over the pairs it flagged (a launch that exits at once when none is).
 template <int D>
-cudaError_t launch_long_dim(const LongArgs& a, int sms, cudaStream_t st, const LongWs& w, int G) {
-  const bool i = a.dtype == 1;
-  if (!i) {
-    if (a.norm == 1) return launch_long_k<K_L1, D, false, F_NONE>(a, sms, st, w, G);
-    if (a.norm == 3) return launch_long_k<K_LINF, D, false, F_NONE>(a, sms, st, w, G);
-    if (a.norm == 2) return launch_long_k<K_SQ, D, false, F_SQRT>(a, sms, st, w, G);
-    return launch_long_k<K_SQ, D, false, F_NONE>(a, sms, st, w, G);
+cudaError_t launch_long_dim(const LongArgs& a, int sms, cudaStream_t st, const LongWs& w, int G,
+                            int64_t* launches) {
+  ++*launches;
+  if (a.dtype != 1) {
+    if (a.norm == 1) return launch_long_k<float, K_L1, D, false, F_NONE>(a, sms, st, w, G);
+    if (a.norm == 3) return launch_long_k<float, K_LINF, D, false, F_NONE>(a, sms, st, w, G);
+    if (a.norm == 2) return launch_long_k<float, K_SQ, D, false, F_SQRT>(a, sms, st, w, G);
+    return launch_long_k<float, K_SQ, D, false, F_NONE>(a, sms, st, w, G);
   }
-  if (a.norm == 4) return launch_long_k<K_XSQ, D, true, F_NONE>(a, sms, st, w, G);
-  if (a.norm == 1) return launch_long_k<K_L1, D, true, F_NONE>(a, sms, st, w, G);
-  return launch_long_k<K_LINF, D, true, F_NONE>(a, sms, st, w, G);
+  cudaError_t e;
+  if (a.norm == 4) e = launch_long_k<float, K_XSQ, D, true, F_NONE>(a, sms, st, w, G);
+  else if (a.norm == 1) e = launch_long_k<float, K_L1, D, true, F_NONE>(a, sms, st, w, G);
+  else e = launch_long_k<float, K_LINF, D, true, F_NONE>(a, sms, st, w, G);
+  if (e != cudaSuccess) return e;
+  ++*launches;
+  if (a.norm == 4) return launch_long_k<long long, K_SQ, D, true, F_NONE>(a, sms, st, w, G);
+  if (a.norm == 1) return launch_long_k<long long, K_L1, D, true, F_NONE>(a, sms, st, w, G);
+  return launch_long_k<long long, K_LINF, D, true, F_NONE>(a, sms, st, w, G);
 }
 
 }  // namespace ffd

@@ -64,10 +64,11 @@ def test_long_pairs_int_exact(ffd):
         assert got[k] == oracle.pair(p, q, "sql2", form="linear")
 
 
-@pytest.mark.parametrize("ctas,expect_ok", [("3", True), ("6", True), ("1", False)])
-def test_long_pair_rows_per_lane(ffd, ctas, expect_ok):
-    """fewer CTAs force R = 32 / 16 (all bands must be co-resident); a pair that does
-    not fit even at R = 32 gets NaN (documented limit)"""
+@pytest.mark.parametrize("ctas", ["3", "6", "1", "2"])
+def test_long_pair_rows_per_lane(ffd, ctas):
+    """Fewer CTAs force taller bands (R = 32 / 16); when even R = 32 does not fit
+    every band at once (1 or 2 CTAs: 40 bands of 512 rows on 8 or 16 slots) the
+    pair runs in several passes chained through the group's wrap link."""
     rng = np.random.default_rng(5)
     pairs = [(walk(rng, 20000), walk(rng, 20000)), (walk(rng, 300), walk(rng, 5000))]
     os.environ["FFD_LONG_CTAS"] = ctas
@@ -75,13 +76,100 @@ def test_long_pair_rows_per_lane(ffd, ctas, expect_ok):
         got = run_pairs(ffd, pairs, "l2")
     finally:
         del os.environ["FFD_LONG_CTAS"]
+    for k, (p, q) in enumerate(pairs):
+        assert got[k] == _mirror_l2(k, p, q), k
     p, q = pairs[0]
-    if expect_ok:
-        assert got[0] == oracle.pair(p, q, "l2", form="mirror")
-    else:
-        assert np.isnan(got[0])
-    p, q = pairs[1]
-    assert got[1] == oracle.pair(p, q, "l2", form="mirror")
+    ref = oracle.pair(p, q, "l2", form="linear")
+    assert abs(got[0] - ref) <= 1e-5 * ref
+
+
+_MIRROR_CACHE = {}
+
+
+def _mirror_l2(k, p, q):
+    if k not in _MIRROR_CACHE:
+        _MIRROR_CACHE[k] = oracle.pair(p, q, "l2", form="mirror")
+    return _MIRROR_CACHE[k]
+
+
+@pytest.mark.parametrize("norm", ["l1", "linf", "sql2"])
+def test_multipass_groups_several_pairs(ffd, norm):
+    """Several multi-pass pairs in one call on one or two CTA groups (tag bases
+    advance by one stream per pass; odd stream lengths; pairs of different pass
+    counts), fp32 and exact int32."""
+    rng = np.random.default_rng(7)
+    shapes = [(9000, 9001), (4100, 12000), (6000, 5999), (700, 20000)]
+    kind = "i" if norm == "sql2" else "f"
+    pairs = [(walk(rng, n, kind=kind), walk(rng, m, kind=kind)) for n, m in shapes]
+    exp = [oracle.pair(p, q, norm, form="mirror" if kind == "f" else "linear") for p, q in pairs]
+    for ctas in ("1", "2"):
+        os.environ["FFD_LONG_CTAS"] = ctas
+        try:
+            got = run_pairs(ffd, pairs, norm)
+        finally:
+            del os.environ["FFD_LONG_CTAS"]
+        for k in range(len(pairs)):
+            assert got[k] == exp[k], (ctas, k, got[k], exp[k])
+
+
+def test_beyond_coresident_rows_closed_form(ffd):
+    """A pair longer than every band the GPU holds at once (148 × 8 × 32 × 32 =
+    1,212,416 rows; round 1 returned NaN): n = m = 1,250,000 under L∞ with
+    q = p + t, whose δ is ‖t‖∞ exactly (the (0,0) cell forces it, the diagonal
+    coupling attains it; integer coordinates are exact in fp32)."""
+    rng = np.random.default_rng(8)
+    n = 1_250_000
+    p = np.cumsum(rng.integers(-1, 2, size=(n, 2)), axis=0).astype(np.float32)
+    q = p + np.array([3.0, -4.0], np.float32)
+    got = run_pairs(ffd, [(p, q)], "linf")
+    assert got[0] == 4.0
+
+
+@pytest.mark.parametrize("norm", ["sql2", "l1", "linf"])
+def test_long_int_pairs_outside_fp32_window(ffd, norm):
+    """≤ 148 int32 pairs above 512 rows (so every pair runs on the long-pair CTA
+    groups) with coordinates spread over ±20000: they leave the fp32-exact window
+    and must be recomputed by the exact int64 tier, bit-exact (round 1 wrote
+    INT64_MIN).  Squared distances reach 3.2e9 > 2^31."""
+    rng = np.random.default_rng(9)
+    pairs = []
+    for _ in range(40):
+        n, m = (int(x) for x in rng.integers(600, 5001, size=2))
+        pairs.append((rng.integers(-20000, 20001, size=(n, 2)).astype(np.int32),
+                      rng.integers(-20000, 20001, size=(m, 2)).astype(np.int32)))
+    # and two walks that stay inside the window (the fp32 tier result is kept)
+    pairs += [(walk(rng, 3000, kind="i"), walk(rng, 2500, kind="i")) for _ in range(2)]
+    got = run_pairs(ffd, pairs, norm)
+    P = np.concatenate([p for p, _ in pairs])
+    Q = np.concatenate([q for _, q in pairs])
+    lp = np.array([len(p) for p, _ in pairs], np.int32)
+    lq = np.array([len(q) for _, q in pairs], np.int32)
+    off = np.concatenate([np.concatenate([[0], np.cumsum(lp)[:-1]]),
+                          np.concatenate([[0], np.cumsum(lq)[:-1]])]).astype(np.int64)
+    exp = oracle.batch(P, Q, off, np.concatenate([lp, lq]), 2, norm, threads=0)
+    bad = np.flatnonzero(got != exp)
+    assert bad.size == 0, (bad[:5], got[bad[:5]], exp[bad[:5]])
+
+
+def test_batch_int_multiband_outside_fp32_window(ffd):
+    """More pairs than SMs, 600–3000 points (multi-band pairs on the batch kernel)
+    with coordinates over ±20000: the batch kernel's exact int64 tier, bit-exact."""
+    rng = np.random.default_rng(10)
+    pairs = []
+    for _ in range(200):
+        n, m = (int(x) for x in rng.integers(600, 3001, size=2))
+        pairs.append((rng.integers(-20000, 20001, size=(n, 3)).astype(np.int32),
+                      rng.integers(-20000, 20001, size=(m, 3)).astype(np.int32)))
+    got = run_pairs(ffd, pairs, "sql2")
+    P = np.concatenate([p for p, _ in pairs])
+    Q = np.concatenate([q for _, q in pairs])
+    lp = np.array([len(p) for p, _ in pairs], np.int32)
+    lq = np.array([len(q) for _, q in pairs], np.int32)
+    off = np.concatenate([np.concatenate([[0], np.cumsum(lp)[:-1]]),
+                          np.concatenate([[0], np.cumsum(lq)[:-1]])]).astype(np.int64)
+    exp = oracle.batch(P, Q, off, np.concatenate([lp, lq]), 3, "sql2", threads=0)
+    bad = np.flatnonzero(got != exp)
+    assert bad.size == 0, (bad[:5], got[bad[:5]], exp[bad[:5]])
 
 
 def test_config5_full_size(ffd):

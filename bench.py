@@ -3,14 +3,23 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ffd|reference]
 
-One "step" = one ffd_batch call over the whole config-2 batch (100k pairs,
-2-D int32, lengths U[128,512], squared L2, exact) with inputs resident in HBM
-(512 MB > 126 MB L2: no L2 flush needed).  Multi-GPU (torchrun, one rank per
-GPU): every rank processes its own 100k-pair shard (weak scaling, no data-path
-collective); time = max over ranks.  Rank 0 prints ONE JSON line.
+Default line (config 2 headline + config 4 beside it, the metric's "batched &
+all-pairs"):
+  * value: one "step" = one ffd_batch call over the whole config-2 batch (100k
+    pairs, 2-D int32, lengths U[128,512], squared L2, exact) with inputs resident
+    in HBM (512 MB > 126 MB L2: no flush needed).  With N GPUs every rank
+    processes its own 100k-pair shard (weak scaling, no data-path collective).
+  * all_pairs: config 4 (20k × 20k curves of 128 points, 2-D fp32 L2): rows of A
+    sharded over the N ranks, each rank's block by ffd_cdist, then one NCCL
+    all_gather_into_tensor of the matrix — INSIDE the timed region (strong
+    scaling).  Its own roofline, e2e and cpu_baseline.
+Times are CUDA events on the launching stream, max over ranks; rank 0 prints
+ONE JSON line.  `--gpus N` without a torchrun environment re-executes itself
+under `python -m torch.distributed.run --nproc-per-node N` (127.0.0.1).
 
---impl reference times the CPU oracle (oracle/, the plain C table DP) on the
-host cores on a bounded sample of the same workload — the slow reference arm.
+--config 1/3/4/5 times that config alone.  --impl reference times the CPU
+oracle (oracle/, the plain C table DP) on the host cores on a bounded sample of
+the same workload — the slow reference arm.
 """
 from __future__ import annotations
 
@@ -44,15 +53,11 @@ ISSUE_PER_CELL = {"f32_d2_sq": 4.0, "xsq_d2": 3.5, "f32_d3_sq": 5.0, "f32_d2_l1"
 CELL_OF_CONFIG = {1: "f32_d2_sq", 2: "xsq_d2", 3: "f32_d3_sq", 4: "f32_d2_sq", 5: "f32_d2_sq"}
 CELL_OF_NORM = {"l1": "f32_d2_l1", "l2": "f32_d2_sq", "linf": "f32_d2_linf"}
 MIX_SOURCE = "profiles/r1_microbench_pipes_v2.jsonl (tools/microbench/pipes.cu mixcells_*)"
-# dram__bytes_read.sum + dram__bytes_write.sum of one launch of the dominant kernel, from the
-# committed ncu captures; --traffic overrides.
-#   c2: profiles/r1_c2_batch_ncu_full_v13.txt, 535.8 MB + 6.8 MB (algorithmic 514.3 MB in + 0.8 MB out)
-#   c3: profiles/r1_traffic_c3.csv, 21.86 GB + 1.60 GB (algorithmic 15.4 GB: the second band of a
-#       pair above 512 rows re-streams its columns and reads the first band's bottom row; at
-#       0.2 TB/s the kernel is nowhere near HBM-bound)
-#   c4: profiles/r1_traffic_c4.csv, 136.3 MB + 1590.8 MB (algorithmic 41 MB in + 1600 MB out)
-#   c5: profiles/r1_traffic_c5.csv (L2 instance), 6.83 MB + 0.02 MB (algorithmic 4.2 MB in)
-TRAFFIC_BYTES = {2: 542.6e6, 3: 23.454e9, 4: 1.7271e9, 5: 6.852e6}
+# roofline.traffic (dram bytes per launch of the dominant kernel) is not measurable inside a plain
+# run; it is null here, and the ncu --set full captures of the same kernels, with their dram
+# bytes against the algorithmic bytes, are committed under profiles/ (named per round).
+TRAFFIC_PROFILES = {2: "profiles/r2_c2_batch_ncu_full.txt", 4: "profiles/r2_c4_cdist_ncu_full.txt",
+                    5: "profiles/r2_c5_long_ncu_full.txt", 3: "profiles/r1_traffic_c3.csv"}
 
 
 L2_FLUSH_BELOW = 256 << 20  # inputs smaller than this could stay in L2 (126 MB) between steps
@@ -210,7 +215,8 @@ def oracle_runner(cfg, target_cells: float, cores: int):
 
 
 def cpu_baseline_line(args, cfg, ws):
-    """The oracle timed on the host cores on a bounded sample (rank 0, N = 1 only)."""
+    """The oracle timed on the host cores on a bounded sample (rank 0, N = 1 only),
+    with all host threads and with one (t1)."""
     if ws != 1 or args.no_cpu_baseline:
         return None
     cores = cpu_cores()
@@ -218,8 +224,14 @@ def cpu_baseline_line(args, cfg, ws):
     t = run()
     if cfg.kind == "long":
         cores = len(cfg.norms)
-    return {"value": ccells / t / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
+    line = {"value": ccells / t / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"{sample} (oracle/ffd_oracle.c), {t:.1f} s"}
+    if cfg.kind != "long":  # the long-pair sample already runs one core per norm
+        run1, c1, sample1 = oracle_runner(cfg, args.cpu_cells / 10, 1)
+        t1 = run1()
+        line["t1"] = {"value": c1 / t1 / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+                      "sample": f"{sample1} (one thread), {t1:.1f} s"}
+    return line
 
 
 def bench_reference(args):
@@ -249,22 +261,46 @@ def bench_reference(args):
     return 0
 
 
-def bench_ffd(args):
-    import torch
-    import torch.distributed as dist
+class Ctx:
+    """Per-process GPU / process-group context shared by the measurements."""
 
-    ws, rank, local = dist_env()
-    if ws > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
-    dev = torch.device("cuda", local if ws > 1 else 0)
-    torch.cuda.set_device(dev)
-    import paper_2404_05708_b200 as ffd
-    ffd.lib()
+    def __init__(self):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.ws, self.rank, local = dist_env()
+        if self.ws > 1:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        self.dev = torch.device("cuda", local if self.ws > 1 else 0)
+        torch.cuda.set_device(self.dev)
+        import paper_2404_05708_b200 as ffd
+        ffd.lib()
+        self.ffd = ffd
+        self.stream = torch.cuda.current_stream(self.dev)
+        self.sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
 
-    cfg = workload.CONFIGS[args.config]
-    assert cfg.kind == "batch", "bench.py times the batch path (configs 1-3)"
-    first = rank * cfg.pairs
+    def barrier(self):
+        if self.ws > 1:
+            self.dist.barrier()
+
+    def reduce(self, vals, op="max"):
+        if self.ws == 1:
+            return list(vals)
+        t = self.torch.tensor(list(vals), dtype=self.torch.float64, device=self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX if op == "max" else self.dist.ReduceOp.SUM)
+        return [float(x) for x in t.tolist()]
+
+    def close(self):
+        if self.ws > 1:
+            self.dist.destroy_process_group()
+
+
+def measure_batch(args, cx, cfg):
+    """A batch config (1-3): every rank its own shard of cfg.pairs pairs (weak
+    scaling, no collective).  Returns the JSON line (rank 0) or None."""
+    torch, ffd, dev, stream = cx.torch, cx.ffd, cx.dev, cx.stream
+    first = cx.rank * cfg.pairs
 
     def pinned(shape, dtype):
         t = torch.empty(shape, dtype=torch.from_numpy(np.zeros(0, dtype)).dtype, pin_memory=True)
@@ -275,39 +311,20 @@ def bench_ffd(args):
     B = b.num_pairs
     p = torch.from_numpy(b.p).to(dev)
     q = torch.from_numpy(b.q).to(dev)
-    off_h = torch.from_numpy(b.offsets).pin_memory()
-    len_h = torch.from_numpy(b.lengths).pin_memory()
-    off = off_h.to(dev)
-    lens = len_h.to(dev)
+    off = torch.from_numpy(b.offsets).to(dev)
+    lens = torch.from_numpy(b.lengths).to(dev)
     out = torch.empty(B, dtype=torch.int64 if cfg.dtype == "i32" else torch.float32, device=dev)
-    stream = torch.cuda.current_stream(dev)
-
-    def barrier():
-        if ws > 1:
-            dist.barrier()
-
-    def max_over_ranks(x: float) -> float:
-        if ws == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    def sum_over_ranks(x: float) -> float:
-        if ws == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
+    # the inputs are generated by workload/ and checked once by the library's own validator
+    assert ffd.validate(p, q, off, lens) == 0
 
     # ---- device-resident timing ------------------------------------------------
     for _ in range(args.warmup):
-        ffd.batch(p, q, off, lens, norm=cfg.norm, out=out)
+        ffd.batch(p, q, off, lens, norm=cfg.norm, out=out, validate=False)
     torch.cuda.synchronize()
     ffd.launches_taken()
     ffd.profile_take()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
+    cx.barrier()
     torch.cuda.synchronize()
     sampler = ClockSampler(dev.index)
     ffd.profile_enable(True)
@@ -317,24 +334,25 @@ def bench_ffd(args):
     with sampler:
         if flush:
             ms = timed_steps_flushed(torch, stream, dev,
-                                     lambda: ffd.batch(p, q, off, lens, norm=cfg.norm, out=out), args.steps)
+                                     lambda: ffd.batch(p, q, off, lens, norm=cfg.norm, out=out, validate=False),
+                                     args.steps)
         else:
             e0.record(stream)
             h0 = time.perf_counter()
             for _ in range(args.steps):
-                ffd.batch(p, q, off, lens, norm=cfg.norm, out=out)
+                ffd.batch(p, q, off, lens, norm=cfg.norm, out=out, validate=False)
             host_ms = (time.perf_counter() - h0) * 1e3 / args.steps
             e1.record(stream)
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / args.steps
     ffd.profile_enable(False)
-    barrier()
+    cx.barrier()
     launches = ffd.launches_taken() // args.steps
     kern_ms_total, kern_n = ffd.profile_take()
     kern_ms = kern_ms_total / max(kern_n, 1)
     checksum = int(out.sum().item()) if cfg.dtype == "i32" else float(out.double().sum().item())
-    ms_max = max_over_ranks(ms)
-    total_cells = sum_over_ranks(float(cells))
+    ms_max, kern_max = cx.reduce([ms, kern_ms])
+    total_cells = cx.reduce([float(cells)], "sum")[0]
     value = total_cells / (ms_max * 1e-3) / 1e9
 
     # ---- the same step replayed from a CUDA graph (small, launch-bound batches):
@@ -346,11 +364,11 @@ def bench_ffd(args):
             side = torch.cuda.Stream(dev)
             side.wait_stream(stream)
             with torch.cuda.stream(side):
-                ffd.batch(p, q, off, lens, norm=cfg.norm, out=out)
+                ffd.batch(p, q, off, lens, norm=cfg.norm, out=out, validate=False)
             stream.wait_stream(side)
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                ffd.batch(p, q, off, lens, norm=cfg.norm, out=out)
+                ffd.batch(p, q, off, lens, norm=cfg.norm, out=out, validate=False)
             for _ in range(args.warmup):
                 g.replay()
             torch.cuda.synchronize()
@@ -364,8 +382,8 @@ def bench_ffd(args):
                 g1.record(stream)
                 torch.cuda.synchronize()
                 g_ms = g0.elapsed_time(g1) / args.steps
-            g_ms = max_over_ranks(g_ms)
-            graph = {"ms_per_step": g_ms, "value": sum_over_ranks(float(cells)) / (g_ms * 1e-3) / 1e9,
+            g_ms = cx.reduce([g_ms])[0]
+            graph = {"ms_per_step": g_ms, "value": total_cells / (g_ms * 1e-3) / 1e9,
                      "unit": "Gcells/s", "api": "ffd_batch captured once into a CUDA graph, replayed per step"}
         except Exception as e:  # reported, never silently replaced
             graph = {"error": f"{type(e).__name__}: {e}"[:200]}
@@ -374,7 +392,7 @@ def bench_ffd(args):
     out_h = torch.empty(B, dtype=out.dtype, pin_memory=True).numpy()
     for _ in range(max(1, min(args.warmup, 2))):
         ffd.batch_host(b.p, b.q, b.offsets, b.lengths, norm=cfg.norm, out=out_h)
-    barrier()
+    cx.barrier()
     torch.cuda.synchronize()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record(stream)
@@ -382,45 +400,39 @@ def bench_ffd(args):
         ffd.batch_host(b.p, b.q, b.offsets, b.lengths, norm=cfg.norm, out=out_h)
     e3.record(stream)
     torch.cuda.synchronize()
-    barrier()
-    e2e_ms = max_over_ranks(e2.elapsed_time(e3) / args.steps)
+    cx.barrier()
+    e2e_ms = cx.reduce([e2.elapsed_time(e3) / args.steps])[0]
     e2e_ok = bool(np.array_equal(out_h, out.cpu().numpy()))
     h2d = b.p.nbytes + b.q.nbytes + b.offsets.nbytes + b.lengths.nbytes
     d2h = out_h.nbytes
-
-    if rank != 0:
-        if ws > 1:
-            dist.destroy_process_group()
-        return 0
+    if cx.rank != 0:
+        return None
 
     clocks = sampler.summary()
     f_meas = (clocks["sm_mhz"] or SM_MAX_MHZ_NOMINAL) * 1e6
     f_max = (clocks["sm_max_mhz"] or SM_MAX_MHZ_NOMINAL) * 1e6
-    sms = torch.cuda.get_device_properties(dev).multi_processor_count
     cell = CELL_OF_CONFIG[cfg.cid]
-    traffic = args.traffic if args.traffic is not None else TRAFFIC_BYTES.get(cfg.cid)
-    roofline = alu_roofline(cells, kern_ms, cell, sms, f_max, f_meas,
-                            f"batch_kernel ({cell} cell)", traffic)
-    roofline["algorithmic_bytes"] = b.p.nbytes + b.q.nbytes + b.offsets.nbytes + b.lengths.nbytes + out.numel() * out.element_size()
-
-    cpu = cpu_baseline_line(args, cfg, ws)
-
+    roofline = alu_roofline(cells, kern_max, cell, cx.sms, f_max, f_meas,
+                            f"batch_kernel ({cell} cell)", None)
+    roofline["algorithmic_bytes"] = h2d + out.numel() * out.element_size()
+    roofline["traffic_ncu"] = TRAFFIC_PROFILES.get(cfg.cid)
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": cx.ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32",
+        "vs_baseline": None, "dtype": "int64" if cfg.dtype == "i32" else "f32",
         "data": "synthetic",
         "config": {"workload": cfg.name, "pairs_per_gpu": B, "cells_per_gpu_step": cells,
-                   "arithmetic": ("fp32 arithmetic, exact for these integers (every partial < 2^24), "
-                                  "int64 results" if cfg.dtype == "i32" else "fp32"),
+                   "arithmetic": ("int32 coordinates, exact int64 results: fp32 instructions on translated "
+                                  "coordinates whose every partial is an integer < 2^24 (exact), int64 tier "
+                                  "for pairs outside that window" if cfg.dtype == "i32" else "fp32"),
                    "dim": cfg.dim, "norm": cfg.norm, "lengths": list(cfg.len_p),
                    "l2": ("L2 flushed (256 MB write) before every timed step; steps timed one by one"
                           if flush else
                           "inputs larger than L2 (%.0f MB per GPU)" % ((b.p.nbytes + b.q.nbytes) / 1e6)),
-                   "parallelism": f"pairs sharded over {ws} GPU(s), no collective on the data path"},
+                   "parallelism": f"pairs sharded over {cx.ws} GPU(s), no collective on the data path"},
         "clocks": clocks,
         "roofline": roofline,
-        "cpu_baseline": cpu,
+        "cpu_baseline": cpu_baseline_line(args, cfg, cx.ws),
         "e2e": {"value": total_cells / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "matches_device_result": e2e_ok,
                 "api": "ffd_batch_host (pinned host buffers, H2D + kernels + D2H per step)"},
@@ -431,27 +443,15 @@ def bench_ffd(args):
     }
     if graph is not None:
         line["graph_replay"] = graph
-    print(json.dumps(line), flush=True)
-    if ws > 1:
-        dist.destroy_process_group()
-    return 0
+    return line
 
 
-def bench_cdist(args):
+def measure_cdist(args, cx, steps):
     """Config 4: all-pairs δ between two sets of 20k curves (L=128), rows of A sharded
-    over ranks, one NCCL all_gather_into_tensor assembles the matrix (SURVEY §8(a) a7+a9)."""
-    import torch
-    import torch.distributed as dist
-
-    ws, rank, local = dist_env()
-    if ws > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
-    dev = torch.device("cuda", local if ws > 1 else 0)
-    torch.cuda.set_device(dev)
-    import paper_2404_05708_b200 as ffd
+    over the ranks, one NCCL all_gather_into_tensor assembles the matrix inside the
+    timed region (SURVEY §8(a) a7 + a9; strong scaling).  Returns a dict (rank 0)."""
+    torch, ffd, dev, stream = cx.torch, cx.ffd, cx.dev, cx.stream
     from paper_2404_05708_b200.dist import assemble, row_range
-    ffd.lib()
     cfg = workload.CONFIGS[4]
     if args.cdist_rows:
         cfg = cfg.scaled(nA=args.cdist_rows)
@@ -459,16 +459,15 @@ def bench_cdist(args):
     B_h = workload.gen_set(cfg, "B")
     A = torch.from_numpy(A_h).to(dev)
     B = torch.from_numpy(B_h).to(dev)
-    r0, r1, blk = row_range(cfg.nA, ws, rank)
+    r0, r1, blk = row_range(cfg.nA, cx.ws, cx.rank)
     block = torch.empty((blk, cfg.nB), dtype=torch.float32, device=dev)
     cells_rank = (r1 - r0) * cfg.nB * cfg.length * cfg.length
     total_cells = cfg.nA * cfg.nB * cfg.length * cfg.length
-    stream = torch.cuda.current_stream(dev)
 
     def step():
         if r1 > r0:
             ffd.cdist(A, B, cfg.norm, rows=(r0, r1), out=block)
-        if ws > 1:
+        if cx.ws > 1:
             return assemble(block, cfg.nA)
         return block
 
@@ -477,75 +476,107 @@ def bench_cdist(args):
     torch.cuda.synchronize()
     ffd.launches_taken()
     ffd.profile_take()
-    if ws > 1:
-        dist.barrier()
+    cx.barrier()
     torch.cuda.synchronize()
     sampler = ClockSampler(dev.index)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ffd.profile_enable(True)
     with sampler:
         e0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(steps):
             full = step()
         e1.record(stream)
         torch.cuda.synchronize()
     ffd.profile_enable(False)
-    ms = e0.elapsed_time(e1) / args.steps
+    cx.barrier()
+    ms = e0.elapsed_time(e1) / steps
     kern_ms_total, kern_n = ffd.profile_take()
     kern_ms = kern_ms_total / max(kern_n, 1)
-    launches = ffd.launches_taken() // args.steps
-    t = torch.tensor([ms, kern_ms], dtype=torch.float64, device=dev)
-    if ws > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max, kern_max = float(t[0]), float(t[1])
+    launches = ffd.launches_taken() // steps
+    ms_max, kern_max = cx.reduce([ms, kern_ms])
     checksum = float(full.double().sum().item())
+    # the gather alone (max over ranks): what the collective adds to the step
+    gather_ms = None
+    if cx.ws > 1:
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        cx.barrier()
+        g0.record(stream)
+        for _ in range(steps):
+            assemble(block, cfg.nA)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gather_ms = cx.reduce([g0.elapsed_time(g1) / steps])[0]
     # end to end: host A, B -> device, compute + gather, full matrix -> host
     out_h = torch.empty((cfg.nA, cfg.nB), dtype=torch.float32, pin_memory=True)
     A_p = torch.from_numpy(A_h).pin_memory()
     B_p = torch.from_numpy(B_h).pin_memory()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if ws > 1:
-        dist.barrier()
+    e2e_steps = max(1, steps // 4)
+    cx.barrier()
     e2.record(stream)
-    for _ in range(max(1, args.steps // 4)):
+    for _ in range(e2e_steps):
         A.copy_(A_p, non_blocking=True)
         B.copy_(B_p, non_blocking=True)
         f = step()
         out_h.copy_(f, non_blocking=True)
     e3.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = e2.elapsed_time(e3) / max(1, args.steps // 4)
-    t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-    if ws > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_ms = float(t[0])
-    if rank == 0:
-        clocks = sampler.summary()
-        f_max = (clocks["sm_max_mhz"] or SM_MAX_MHZ_NOMINAL) * 1e6
-        f_meas = (clocks["sm_mhz"] or SM_MAX_MHZ_NOMINAL) * 1e6
-        sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        line = {
-            "metric": METRIC, "value": total_cells / (ms_max * 1e-3) / 1e9, "unit": UNIT, "n_gpus": ws,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg.name, "nA": cfg.nA, "nB": cfg.nB, "length": cfg.length,
-                       "cells_per_step": total_cells, "norm": cfg.norm,
-                       "parallelism": f"rows of A over {ws} GPU(s) + all_gather_into_tensor (NCCL)",
-                       "l2": "every step writes the 1.6 GB output, which evicts L2 between steps; B (20 MB) is L2-resident within a step by design"},
-            "clocks": clocks,
-            "cpu_baseline": cpu_baseline_line(args, cfg, ws),
-            "roofline": alu_roofline(cells_rank, kern_max, CELL_OF_CONFIG[4], sms, f_max, f_meas,
-                                     "cdist_kernel (fp32 L2, W=4 R=32)",
-                                     args.traffic if args.traffic is not None else TRAFFIC_BYTES.get(4)),
-            "e2e": {"value": total_cells / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
-                    "h2d_bytes_per_step": A_h.nbytes + B_h.nbytes,
-                    "d2h_bytes_per_step": cfg.nA * cfg.nB * 4},
-            "gpu_launches": launches * args.steps, "gpu_launches_per_step": launches,
-            "checksum": checksum,
-        }
+    e2e_ms = cx.reduce([e2.elapsed_time(e3) / e2e_steps])[0]
+    if cx.rank != 0:
+        return None
+    clocks = sampler.summary()
+    f_max = (clocks["sm_max_mhz"] or SM_MAX_MHZ_NOMINAL) * 1e6
+    f_meas = (clocks["sm_mhz"] or SM_MAX_MHZ_NOMINAL) * 1e6
+    roofline = alu_roofline(cells_rank, kern_max, CELL_OF_CONFIG[4], cx.sms, f_max, f_meas,
+                            "cdist_kernel (fp32 L2, W=4 R=32)", None)
+    roofline["algorithmic_bytes"] = A_h.nbytes + B_h.nbytes + (r1 - r0) * cfg.nB * 4
+    roofline["traffic_ncu"] = TRAFFIC_PROFILES.get(4)
+    return {
+        "metric": METRIC, "value": total_cells / (ms_max * 1e-3) / 1e9, "unit": UNIT, "n_gpus": cx.ws,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+        "scaling": "strong", "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg.name, "nA": cfg.nA, "nB": cfg.nB, "length": cfg.length,
+                   "cells_per_step": total_cells, "norm": cfg.norm,
+                   "parallelism": f"rows of A over {cx.ws} GPU(s) + all_gather_into_tensor (NCCL) in the step",
+                   "l2": "every step writes the 1.6 GB output, which evicts L2 between steps; "
+                         "B (20 MB) is L2-resident within a step by design"},
+        "clocks": clocks,
+        "kernel_ms_per_rank": kern_max,
+        "all_gather_ms": gather_ms,
+        "cpu_baseline": cpu_baseline_line(args, cfg, cx.ws),
+        "roofline": roofline,
+        "e2e": {"value": total_cells / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": A_h.nbytes + B_h.nbytes,
+                "d2h_bytes_per_step": cfg.nA * cfg.nB * 4,
+                "api": "dist.cdist path: H2D of A and B, ffd_cdist per rank, all-gather, D2H of the matrix"},
+        "gpu_launches": launches * steps, "gpu_launches_per_step": launches,
+        "checksum": checksum,
+    }
+
+
+def bench_ffd(args):
+    """The default line: config 2 (headline value) with config 4 beside it."""
+    cx = Ctx()
+    cfg = workload.CONFIGS[args.config]
+    line = measure_batch(args, cx, cfg)
+    if args.config == 2 and not args.no_cdist:
+        ap = measure_cdist(args, cx, args.steps)
+        if line is not None:
+            line["all_pairs"] = ap
+            line["gpu_launches_all_pairs"] = ap["gpu_launches"]
+    if line is not None:
         print(json.dumps(line), flush=True)
-    if ws > 1:
-        dist.destroy_process_group()
+    cx.close()
+    return 0
+
+
+def bench_cdist(args):
+    cx = Ctx()
+    line = measure_cdist(args, cx, args.steps)
+    if line is not None:
+        line["vs_baseline"] = None
+        print(json.dumps(line), flush=True)
+    cx.close()
     return 0
 
 
@@ -629,9 +660,7 @@ def bench_long(args):
         # waiting for SMs) must not stand for the kernel
         kern = {nm: float(np.median(per_norm[nm])) for nm in cfg.norms}
         per = {nm: alu_roofline(cells, kern[nm], CELL_OF_NORM[nm], sms, f_max, f_meas,
-                                f"long_kernel (fp32 {nm})",
-                                args.traffic if args.traffic is not None
-                                else (TRAFFIC_BYTES.get(5) if nm == "l2" else None)) for nm in cfg.norms}
+                                f"long_kernel (fp32 {nm})", None) for nm in cfg.norms}
         line = {
             "metric": METRIC, "value": ws * 3 * cells / (ms_max * 1e-3) / 1e9, "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
@@ -655,6 +684,19 @@ def bench_long(args):
     return 0
 
 
+def spawn_ranks(n: int):
+    """Re-execute this command under torchrun with n ranks on this node (127.0.0.1)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)]
+    cmd += [a for a in sys.argv[1:] if a != "--spawn"]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -664,12 +706,18 @@ def main():
     ap.add_argument("--impl", default="ffd", choices=["ffd", "reference"])
     ap.add_argument("--cpu-cells", type=float, default=3e9, help="cells in the oracle cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cdist", action="store_true", help="default line: skip the config-4 all_pairs leg")
     ap.add_argument("--cdist-rows", type=int, default=0, help="config 4: use only this many A curves")
-    ap.add_argument("--traffic", type=float, default=None,
-                    help="dram bytes per launch of the dominant kernel from an ncu --set full capture")
+    ap.add_argument("--spawn", action="store_true",
+                    help="run under torchrun even for --gpus 1 (the multi-rank launch path)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if "WORLD_SIZE" not in os.environ and (args.gpus > 1 or args.spawn):
+        spawn_ranks(args.gpus)  # does not return
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; timing {ws} rank(s)", file=sys.stderr)
     if args.impl == "reference":
         return bench_reference(args)
     kind = workload.CONFIGS[args.config].kind

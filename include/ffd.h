@@ -156,6 +156,30 @@ int ffd_cdist_self(const void* setA, int64_t nA, int32_t lenA, int32_t dim, int3
                    int32_t dtype, int64_t row_begin, int64_t row_end, void* out, int64_t ld_out,
                    void* workspace, size_t workspace_bytes, ffd_stream_t stream);
 
+/* ffd_cdist_to — the all-pairs block written straight into one or more FULL
+ *   matrices: this GPU's and, through NVLink, its peers' (north_star (3): the
+ *   fused distribution that replaces the trailing all-gather).
+ *   Rows a ∈ [row_begin, row_end) of setA against the nB curves of setB, whose
+ *   curve b is column col_offset + b.  Every result goes to
+ *     outs_host[i][a*ld_out + col_offset + b]   for i < n_outs (≤ 8),
+ *   and, with mirror = 1, also to outs_host[i][(col_offset + b)*ld_out + a]
+ *   (δ is symmetric: the lower triangle of a self matrix).
+ *   self = 1: setB is setA's rows [col_offset, col_offset + nB) (lenB = lenA);
+ *   each unordered pair with both curves inside [row_begin, row_end) is
+ *   evaluated once and written to both places, as ffd_cdist_self.
+ *   outs_host: a HOST array of n_outs DEVICE pointers — local memory or peer
+ *   memory mapped into this context (CUDA IPC / symmetric memory) — each the
+ *   base of a row-major matrix with ld_out elements per row, owned by the
+ *   caller.  The kernel ends with a system-scope fence, so that a barrier
+ *   sequenced after it on `stream` (e.g. an NCCL all-reduce or a symmetric-
+ *   memory barrier) publishes the results to every peer.  Same dtype / norm /
+ *   workspace / stream rules as ffd_cdist.                                     */
+int ffd_cdist_to(const void* setA, int64_t nA, int32_t lenA, const void* setB, int64_t nB,
+                 int32_t lenB, int32_t dim, int32_t norm, int32_t dtype, int64_t row_begin,
+                 int64_t row_end, int32_t self, int64_t col_offset, int32_t mirror,
+                 void* const* outs_host, int32_t n_outs, int64_t ld_out, void* workspace,
+                 size_t workspace_bytes, ffd_stream_t stream);
+
 /* ---------------------------------------------------------------------------
  * ffd_validate_batch — SYNCHRONOUS device-data precondition check of a batch:
  *   lengths ≥ 1 (FFD_ERR_EMPTY), offsets+lengths within [0, np)/[0, nq)

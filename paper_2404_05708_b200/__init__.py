@@ -11,6 +11,9 @@ missing, calls raise.
     dist_sum(p, q, offsets, lengths, norm)     -> Tensor[B] f64 (ffd_dist_sum)
     batch_host(p, q, offsets, lengths, norm)   -> ndarray[B]  (ffd_batch_host)
     cdist(A, B, norm, rows=None)               -> Tensor      (ffd_cdist)
+    cdist_self(A, norm, rows=None)             -> Tensor      (ffd_cdist_self)
+    cdist_to(A, B, outs, ...)                  -> None        (ffd_cdist_to: results into
+                                                   full matrices on this GPU and NVLink peers)
     validate(p, q, offsets, lengths)           -> status      (ffd_validate_batch)
 """
 from __future__ import annotations
@@ -63,6 +66,9 @@ def lib():
         L.ffd_cdist.restype = ctypes.c_int
         L.ffd_cdist_self.argtypes = [P, I64, I32_, I32_, I32_, I32_, I64, I64, P, I64, P, SZ, P]
         L.ffd_cdist_self.restype = ctypes.c_int
+        L.ffd_cdist_to.argtypes = [P, I64, I32_, P, I64, I32_, I32_, I32_, I32_, I64, I64, I32_, I64, I32_,
+                                   ctypes.POINTER(ctypes.c_void_p), I32_, I64, P, SZ, P]
+        L.ffd_cdist_to.restype = ctypes.c_int
         L.ffd_cdist_workspace_bytes.argtypes = []
         L.ffd_cdist_workspace_bytes.restype = SZ
         L.ffd_validate_batch.argtypes = [P, I64, P, I64, P, P, I64, I32_, I32_, P]
@@ -81,7 +87,7 @@ def lib():
 
 
 EXPORTED = ["ffd_batch", "ffd_batch_dtw", "ffd_dist_sum", "ffd_batch_workspace_bytes", "ffd_batch_host", "ffd_cdist",
-            "ffd_cdist_workspace_bytes", "ffd_cdist_self", "ffd_validate_batch", "ffd_status_string",
+            "ffd_cdist_workspace_bytes", "ffd_cdist_self", "ffd_cdist_to", "ffd_validate_batch", "ffd_status_string",
             "ffd_take_launch_count", "ffd_version", "ffd_profile_enable", "ffd_profile_take"]
 
 
@@ -151,26 +157,44 @@ def launches_taken() -> int:
     return int(lib().ffd_take_launch_count())
 
 
-def batch(p, q, offsets, lengths, norm="l2", out=None, stream=None, measure="frechet"):
-    """δ_dF for B pairs (ffd_batch).  p [Σn, dim], q [Σm, dim] float32/int32 CUDA
-    tensors; offsets int64[2B]; lengths int32[2B].  Returns float32[B] (fp32
-    input) or int64[B] (int32 input).  measure="dtw": dynamic time warping
-    (ffd_batch_dtw, PAPER Appendix B; float32 input only)."""
+def _batch_args(p, q, offsets, lengths):
+    """Common marshalling of the batch layout: dtypes, devices, shapes, contiguity."""
     torch = _torch()
     if not (p.is_cuda and q.is_cuda and offsets.is_cuda and lengths.is_cuda):
         raise ValueError("batch() takes CUDA tensors; use batch_host() for host arrays")
     dt = _dtype_code(p)
     if q.dtype != p.dtype or offsets.dtype != torch.int64 or lengths.dtype != torch.int32:
         raise TypeError("dtype mismatch (p/q same dtype, offsets int64, lengths int32)")
-    p, q = p.contiguous(), q.contiguous()
+    if p.dim() != 2 or q.dim() != 2 or p.shape[1] != q.shape[1]:
+        raise ValueError(f"p and q must be [points, dim] with the same dim, got {tuple(p.shape)}, {tuple(q.shape)}")
+    if offsets.numel() % 2 or offsets.numel() != lengths.numel():
+        raise ValueError("offsets and lengths must both hold 2*B entries")
+    return dt, p.contiguous(), q.contiguous(), offsets.contiguous(), lengths.contiguous()
+
+
+def batch(p, q, offsets, lengths, norm="l2", out=None, stream=None, measure="frechet", validate=True):
+    """δ_dF for B pairs (ffd_batch).  p [Σn, dim], q [Σm, dim] float32/int32 CUDA
+    tensors; offsets int64[2B]; lengths int32[2B].  Returns float32[B] (fp32
+    input) or int64[B] (int32 input).  measure="dtw": dynamic time warping
+    (ffd_batch_dtw, PAPER Appendix B; float32 input only).  validate=True first
+    runs ffd_validate_batch (synchronous) and raises FFDError on empty curves,
+    offsets out of range, non-finite coordinates or int64 overflow; with
+    validate=False such pairs give NaN / INT64_MIN (or are undefined).  Inside a
+    CUDA-graph capture the (synchronous) validation is skipped."""
+    torch = _torch()
+    dt, p, q, offsets, lengths = _batch_args(p, q, offsets, lengths)
     B = offsets.numel() // 2
     dim = p.shape[1]
+    if measure not in ("frechet", "dtw"):
+        raise ValueError(f"unknown measure {measure!r}")
+    if validate and not torch.cuda.is_current_stream_capturing():  # (a synchronous check cannot be captured)
+        _check(int(lib().ffd_validate_batch(p.data_ptr(), p.shape[0], q.data_ptr(), q.shape[0],
+                                            offsets.data_ptr(), lengths.data_ptr(), B, dim, dt,
+                                            _stream_ptr(stream))), "ffd_validate_batch")
     if out is None:
         out = torch.empty(B, dtype=torch.int64 if dt == I32 else torch.float32, device=p.device)
     ws_bytes = lib().ffd_batch_workspace_bytes(B)
     ws = workspace(ws_bytes, p.device, stream)
-    if measure not in ("frechet", "dtw"):
-        raise ValueError(f"unknown measure {measure!r}")
     fn = lib().ffd_batch if measure == "frechet" else lib().ffd_batch_dtw
     _check(fn(p.data_ptr(), q.data_ptr(), offsets.data_ptr(), lengths.data_ptr(), B, dim,
               _norm(norm), dt, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)),
@@ -178,9 +202,9 @@ def batch(p, q, offsets, lengths, norm="l2", out=None, stream=None, measure="fre
     return out
 
 
-def dtw_batch(p, q, offsets, lengths, norm="l2", out=None, stream=None):
+def dtw_batch(p, q, offsets, lengths, norm="l2", out=None, stream=None, validate=True):
     """Dynamic time warping of B pairs (ffd_batch_dtw): same layout as batch()."""
-    return batch(p, q, offsets, lengths, norm=norm, out=out, stream=stream, measure="dtw")
+    return batch(p, q, offsets, lengths, norm=norm, out=out, stream=stream, measure="dtw", validate=validate)
 
 
 def dist_sum(p, q, offsets, lengths, norm="l2", out=None, stream=None):
@@ -189,9 +213,7 @@ def dist_sum(p, q, offsets, lengths, norm="l2", out=None, stream=None):
     torch = _torch()
     if _dtype_code(p) != F32:
         raise FFDError(-2, "ffd_dist_sum")
-    p, q = p.contiguous(), q.contiguous()
-    offsets = offsets.contiguous()
-    lengths = lengths.contiguous()
+    _, p, q, offsets, lengths = _batch_args(p, q, offsets, lengths)
     B = offsets.shape[0] // 2
     if out is None:
         out = torch.empty(B, dtype=torch.float64, device=p.device)
@@ -258,9 +280,35 @@ def cdist_self(A, norm="l2", rows=None, out=None, ld_out=None, stream=None):
     return out
 
 
+def cdist_to(A, B, outs, ld_out, norm="l2", rows=None, self_mode=False, col_offset=0, mirror=False,
+             stream=None):
+    """ffd_cdist_to: rows [r0, r1) of A against the curves of B (column col_offset + b)
+    written straight into every matrix of `outs` — device pointers (ints) of full
+    row-major matrices with ld_out elements per row: this GPU's and NVLink peers'
+    (symmetric memory / CUDA IPC).  mirror=True also writes the transposed place;
+    self_mode=True: B is A's rows [col_offset, col_offset + nB), each unordered pair
+    inside the shard evaluated once."""
+    dt = _dtype_code(A)
+    if B.dtype != A.dtype:
+        raise TypeError("A and B must have the same dtype")
+    A, B = A.contiguous(), B.contiguous()
+    nA, lenA, dim = A.shape
+    nB, lenB, dimB = B.shape
+    if dimB != dim:
+        raise ValueError("A and B must have the same dim")
+    r0, r1 = (0, nA) if rows is None else rows
+    ptrs = (ctypes.c_void_p * len(outs))(*[int(x) for x in outs])
+    wsb = lib().ffd_cdist_workspace_bytes()
+    ws = workspace(wsb, A.device, stream) if wsb else None
+    _check(lib().ffd_cdist_to(A.data_ptr(), nA, lenA, B.data_ptr(), nB, lenB, dim, _norm(norm), dt, r0, r1,
+                              1 if self_mode else 0, col_offset, 1 if mirror else 0, ptrs, len(outs), ld_out,
+                              ws.data_ptr() if ws is not None else None, wsb, _stream_ptr(stream)),
+           "ffd_cdist_to")
+
+
 def validate(p, q, offsets, lengths, stream=None) -> int:
     """ffd_validate_batch (synchronous); returns the status code."""
-    dt = _dtype_code(p)
+    dt, p, q, offsets, lengths = _batch_args(p, q, offsets, lengths)
     B = offsets.numel() // 2
     return int(lib().ffd_validate_batch(p.data_ptr(), p.shape[0], q.data_ptr(), q.shape[0], offsets.data_ptr(),
                                         lengths.data_ptr(), B, p.shape[1], dt, _stream_ptr(stream)))

@@ -258,14 +258,21 @@ __global__ void cdist_pairs_kernel(int64_t first, int64_t n, int64_t row_begin, 
   }
 }
 
+// results of pairs [first, first + n) of the row-major (rows × nB) block to every
+// destination of `d` (and, with d.mirror, to the transposed places)
 template <typename O>
-__global__ void cdist_scatter_kernel(int64_t first, int64_t n, int64_t nB, const O* src, O* out,
-                                     int64_t ld_out) {
+__global__ void cdist_scatter_kernel(int64_t first, int64_t n, int64_t row_begin, int64_t nB, const O* src,
+                                     OutSpec d) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x) {
     const int64_t idx = first + k;
-    out[(idx / nB) * ld_out + idx % nB] = src[k];
+    const int64_t a = row_begin + idx / nB, b = d.col_off + idx % nB;
+    for (int i = 0; i < d.n; i++) {
+      reinterpret_cast<O*>(d.out[i])[(a - d.row_base) * d.ld + b] = src[k];
+      if (d.mirror) reinterpret_cast<O*>(d.out[i])[(b - d.row_base) * d.ld + a] = src[k];
+    }
   }
+  if (d.n > 1) __threadfence_system();
 }
 
 static int cdist_via_batch(const CdistArgs& a, cudaStream_t st) {
@@ -294,11 +301,10 @@ static int cdist_via_batch(const CdistArgs& a, cudaStream_t st) {
     if (rc != FFD_OK) break;
     if (osz == 8)
       cdist_scatter_kernel<long long><<<blocks, 256, 0, st>>>(
-          first, n, a.nB, reinterpret_cast<const long long*>(tmp), reinterpret_cast<long long*>(a.out),
-          a.ld_out);
+          first, n, a.row_begin, a.nB, reinterpret_cast<const long long*>(tmp), a.dst);
     else
-      cdist_scatter_kernel<float><<<blocks, 256, 0, st>>>(first, n, a.nB, reinterpret_cast<const float*>(tmp),
-                                                          reinterpret_cast<float*>(a.out), a.ld_out);
+      cdist_scatter_kernel<float><<<blocks, 256, 0, st>>>(first, n, a.row_begin, a.nB,
+                                                          reinterpret_cast<const float*>(tmp), a.dst);
     ++g_launches;
     if (cudaGetLastError() != cudaSuccess) rc = FFD_ERR_CUDA;
   }
@@ -542,16 +548,18 @@ int ffd_batch_host(const void* p_host, int64_t np, const void* q_host, int64_t n
 
 size_t ffd_cdist_workspace_bytes(void) { return cdist_workspace_bytes(); }
 
-int ffd_cdist(const void* setA, int64_t nA, int32_t lenA, const void* setB, int64_t nB,
-              int32_t lenB, int32_t dim, int32_t norm, int32_t dtype, int64_t row_begin,
-              int64_t row_end, void* out, int64_t ld_out, void* workspace, size_t workspace_bytes,
-              ffd_stream_t stream) {
+static int cdist_common(const void* setA, int64_t nA, int32_t lenA, const void* setB, int64_t nB,
+                        int32_t lenB, int32_t dim, int32_t norm, int32_t dtype, int64_t row_begin,
+                        int64_t row_end, int self, const OutSpec& dst, void* workspace,
+                        size_t workspace_bytes, ffd_stream_t stream) {
   int s = check_common(dim, norm, dtype);
   if (s) return s;
   if (nA < 0 || nB < 0 || row_begin < 0 || row_end < row_begin || row_end > nA) return FFD_ERR_ARG;
-  if (ld_out < nB) return FFD_ERR_ARG;
+  if (dst.n < 1 || dst.n > kMaxOuts || dst.col_off < 0 || dst.row_base < 0) return FFD_ERR_ARG;
   if (row_end == row_begin || nB == 0) return FFD_OK;
-  if (!setA || !setB || !out || lenA < 1 || lenB < 1) return FFD_ERR_ARG;
+  if (!setA || !setB || lenA < 1 || lenB < 1) return FFD_ERR_ARG;
+  for (int i = 0; i < dst.n; i++)
+    if (!dst.out[i]) return FFD_ERR_ARG;
   if (workspace_bytes < cdist_workspace_bytes() || (!workspace && cdist_workspace_bytes() > 0))
     return FFD_ERR_WORKSPACE;
   CdistArgs a{};
@@ -566,42 +574,60 @@ int ffd_cdist(const void* setA, int64_t nA, int32_t lenA, const void* setB, int6
   a.dtype = dtype;
   a.row_begin = row_begin;
   a.row_end = row_end;
-  a.out = out;
-  a.ld_out = ld_out;
+  a.dst = dst;
   a.workspace = workspace;
+  a.self = self;
   ProfScope prof(reinterpret_cast<cudaStream_t>(stream), 3);
   return cdist_dispatch(a, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ffd_cdist(const void* setA, int64_t nA, int32_t lenA, const void* setB, int64_t nB,
+              int32_t lenB, int32_t dim, int32_t norm, int32_t dtype, int64_t row_begin,
+              int64_t row_end, void* out, int64_t ld_out, void* workspace, size_t workspace_bytes,
+              ffd_stream_t stream) {
+  if (ld_out < nB) return FFD_ERR_ARG;
+  if (!out && row_end > row_begin && nB > 0) return FFD_ERR_ARG;
+  OutSpec d{};
+  d.out[0] = out;
+  d.n = 1;
+  d.row_base = row_begin;
+  d.ld = ld_out;
+  return cdist_common(setA, nA, lenA, setB, nB, lenB, dim, norm, dtype, row_begin, row_end, 0, d,
+                      workspace, workspace_bytes, stream);
 }
 
 int ffd_cdist_self(const void* setA, int64_t nA, int32_t lenA, int32_t dim, int32_t norm,
                    int32_t dtype, int64_t row_begin, int64_t row_end, void* out, int64_t ld_out,
                    void* workspace, size_t workspace_bytes, ffd_stream_t stream) {
-  int s = check_common(dim, norm, dtype);
-  if (s) return s;
-  if (nA < 0 || row_begin < 0 || row_end < row_begin || row_end > nA) return FFD_ERR_ARG;
   if (ld_out < nA) return FFD_ERR_ARG;
-  if (row_end == row_begin) return FFD_OK;
-  if (!setA || !out || lenA < 1) return FFD_ERR_ARG;
-  if (workspace_bytes < cdist_workspace_bytes() || (!workspace && cdist_workspace_bytes() > 0))
-    return FFD_ERR_WORKSPACE;
-  CdistArgs a{};
-  a.A = setA;
-  a.B = setA;
-  a.nA = nA;
-  a.nB = nA;
-  a.lenA = lenA;
-  a.lenB = lenA;
-  a.dim = dim;
-  a.norm = norm;
-  a.dtype = dtype;
-  a.row_begin = row_begin;
-  a.row_end = row_end;
-  a.out = out;
-  a.ld_out = ld_out;
-  a.workspace = workspace;
-  a.self = 1;
-  ProfScope prof(reinterpret_cast<cudaStream_t>(stream), 3);
-  return cdist_dispatch(a, reinterpret_cast<cudaStream_t>(stream));
+  if (!out && row_end > row_begin) return FFD_ERR_ARG;
+  OutSpec d{};
+  d.out[0] = out;
+  d.n = 1;
+  d.row_base = row_begin;
+  d.ld = ld_out;
+  return cdist_common(setA, nA, lenA, setA, nA, lenA, dim, norm, dtype, row_begin, row_end, 1, d,
+                      workspace, workspace_bytes, stream);
+}
+
+int ffd_cdist_to(const void* setA, int64_t nA, int32_t lenA, const void* setB, int64_t nB,
+                 int32_t lenB, int32_t dim, int32_t norm, int32_t dtype, int64_t row_begin,
+                 int64_t row_end, int32_t self, int64_t col_offset, int32_t mirror,
+                 void* const* outs_host, int32_t n_outs, int64_t ld_out, void* workspace,
+                 size_t workspace_bytes, ffd_stream_t stream) {
+  if (!outs_host || n_outs < 1 || n_outs > kMaxOuts) return FFD_ERR_ARG;
+  if (self && mirror) return FFD_ERR_ARG;
+  if (self && lenB != lenA) return FFD_ERR_ARG;  // self: B is A's rows [col_offset, col_offset + nB)
+  if (ld_out < col_offset + nB || (mirror && ld_out < nA) || (self && ld_out < nA)) return FFD_ERR_ARG;
+  OutSpec d{};
+  for (int i = 0; i < n_outs; i++) d.out[i] = outs_host[i];
+  d.n = n_outs;
+  d.row_base = 0;
+  d.col_off = col_offset;
+  d.ld = ld_out;
+  d.mirror = mirror ? 1 : 0;
+  return cdist_common(setA, nA, lenA, setB, nB, lenB, dim, norm, dtype, row_begin, row_end, self ? 1 : 0, d,
+                      workspace, workspace_bytes, stream);
 }
 
 int ffd_validate_batch(const void* p, int64_t np, const void* q, int64_t nq,

@@ -37,13 +37,19 @@ struct CdistProblem {
   int64_t nA, nB;
   int lenA, lenB;
   int64_t row_begin, row_end;
-  float* out;
-  int64_t ld_out;
+  OutSpec dst;
   int* counter;
   int64_t n_items;
   int64_t tiles_b;
   int self;  // B is A (ffd_cdist_self): evaluate each unordered pair once inside the shard
 };
+
+// one result to every destination (local matrix and/or NVLink peer matrices)
+__device__ __forceinline__ void put_result(const OutSpec& d, int64_t row, int64_t col, float v) {
+#pragma unroll 1
+  for (int i = 0; i < d.n; i++)
+    reinterpret_cast<float*>(d.out[i])[(row - d.row_base) * d.ld + col] = v;
+}
 
 constexpr int kCdMinCtasPerSm = 4;  // 128 registers/thread: the W=8, R=16 shape needs ~100
                                     // (R = 32 shapes: 3 CTAs/SM, 168 registers)
@@ -77,7 +83,8 @@ __global__ void __launch_bounds__(kWarp* kWarpsPerCta, (R > 16) ? 3 : kCdMinCtas
       // every (a, b) of this item has b < a with b inside the shard: it is written
       // by the mirror of (b, a) — skip the whole item (δ is symmetric)
       const int64_t a_first = pb.row_begin + ablk * SEG;
-      if (b0 + nb <= a_first && b0 >= pb.row_begin) continue;
+      const int64_t bb0 = pb.dst.col_off + b0;  // B index → A index
+      if (bb0 + nb <= a_first && bb0 >= pb.row_begin) continue;
     }
     const int S = nb * P + 1;                                  // stream positions
 
@@ -181,11 +188,11 @@ __global__ void __launch_bounds__(kWarp* kWarpsPerCta, (R > 16) ? 3 : kCdMinCtas
         if (s == W - 1 && a_ok) {
           float v = c[R - 1];
           if constexpr (FIN == F_SQRT) v = __fsqrt_rn(v);
-          const int64_t b = b0 + out_b;
+          const int64_t b = pb.dst.col_off + b0 + out_b;  // column of the result
           const bool in_shard = pb.self && b >= pb.row_begin && b < pb.row_end;
           // self mode: (a, b) with b < a inside the shard is the mirror's job
-          if (!(in_shard && b < a)) pb.out[(a - pb.row_begin) * pb.ld_out + b] = v;
-          if (in_shard && b > a) pb.out[(b - pb.row_begin) * pb.ld_out + a] = v;
+          if (!(in_shard && b < a)) put_result(pb.dst, a, b, v);
+          if ((in_shard && b > a) || (pb.dst.mirror && !pb.self)) put_result(pb.dst, b, a, v);
         }
         ++out_b;
         next_out += P;
@@ -198,6 +205,9 @@ __global__ void __launch_bounds__(kWarp* kWarpsPerCta, (R > 16) ? 3 : kCdMinCtas
     }
     __syncwarp();
   }
+  // results stored into NVLink peers' matrices: order them before whatever the
+  // host sequences after this kernel (the barrier that publishes the matrix)
+  if (pb.dst.n > 1) __threadfence_system();
 }
 
 // ---- dispatch ----------------------------------------------------------------
@@ -259,8 +269,7 @@ int launch_cdist(const CdistArgs& a, int sms, cudaStream_t st, int64_t* launches
   pb.lenB = a.lenB;
   pb.row_begin = a.row_begin;
   pb.row_end = a.row_end;
-  pb.out = reinterpret_cast<float*>(a.out);
-  pb.ld_out = a.ld_out;
+  pb.dst = a.dst;
   pb.counter = reinterpret_cast<int*>(a.workspace);
   pb.self = a.self;
   const int seg = kWarp / W;

@@ -464,15 +464,16 @@ struct LongRunner {
 
 // Rows per lane for a pair whose rows curve has n points, on a group of G
 // co-resident CTAs: the smallest built R whose bands all fit at once
-// (⌈bands / 8⌉ ≤ G: one pass, returns true); else false and the multi-pass R
-// (R = 32 spills; 16 does not).
+// (⌈bands / 8⌉ ≤ G: one pass, returns true); else false and the multi-pass R.
+// (R = 32 is not built: its registers spilled and, the kernel's register count
+// being the maximum over its R paths, slowed every R.)
 template <typename T>
 __host__ __device__ inline bool long_rows_fit(int n, int G, int& R) {
   constexpr bool F = std::is_same<T, float>::value;
-  const int rs_f[5] = {4, 7, 8, 16, 32};  // the R the fp32 tier is built for
-  const int rs_i[2] = {4, 8};             // the R the int64 tier is built for
+  const int rs_f[4] = {4, 7, 8, 16};  // the R the fp32 tier is built for
+  const int rs_i[2] = {4, 8};         // the R the int64 tier is built for
   const int* rs = F ? rs_f : rs_i;
-  const int nr = F ? 5 : 2;
+  const int nr = F ? 4 : 2;
   for (int i = 0; i < nr; i++) {
     R = rs[i];
     const int nb = (n + kWarp * R - 1) / (kWarp * R);
@@ -681,11 +682,8 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
           } else if (R == 8) {
             LongRunner<T, KIND, D, INT_IN, FIN, 8> run{rings[warp], pb, lane};
             go(run);
-          } else if (R == 16) {
-            LongRunner<T, KIND, D, INT_IN, FIN, 16> run{rings[warp], pb, lane};
-            go(run);
           } else {
-            LongRunner<T, KIND, D, INT_IN, FIN, 32> run{rings[warp], pb, lane};
+            LongRunner<T, KIND, D, INT_IN, FIN, 16> run{rings[warp], pb, lane};
             go(run);
           }
         }

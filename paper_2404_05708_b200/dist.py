@@ -1,12 +1,20 @@
-"""Multi-GPU all-pairs distances: row shards of A per rank + one all-gather.
+"""Multi-GPU all-pairs distances: row shards of A per rank, then the matrix on every rank.
 
-ffd_cdist is embarrassingly parallel over output rows: rank r
-computes rows [r·⌈nA/W⌉, (r+1)·⌈nA/W⌉) of the [nA, nB] matrix against all of B
-(B is replicated, 20 MB for config 4), then one
-``all_gather_into_tensor`` over NCCL (NVLink 5 / NVSwitch) assembles the full
-matrix on every rank.  The gather is the only collective; blocks are padded to
-equal height so a single all-gather suffices, and the result is identical bit
-for bit for any world size (δ only selects values).
+ffd_cdist is embarrassingly parallel over output rows (PAPER L259:
+the pairs are independent): rank r computes rows [r·⌈nA/W⌉, (r+1)·⌈nA/W⌉) of the
+[nA, nB] matrix against all of B (B is replicated, 20 MB for config 4).  The result
+is identical bit for bit for any world size (δ only selects values).  Two ways to
+put the full matrix on every rank:
+
+  * distribution="allgather": each rank writes its block locally, then one
+    ``all_gather_into_tensor`` over NCCL (NVLink 5 / NVSwitch) assembles the
+    matrix (blocks padded to equal height so that a single call suffices).
+  * distribution="p2p" (fused): the matrix lives in torch symmetric memory; every
+    rank's kernel (ffd_cdist_to) stores each finished result straight into ALL
+    ranks' matrices through NVLink peer pointers while it computes, so the
+    transfer overlaps the DP tile by tile and no collective moves the matrix.
+    One device-side barrier (the symmetric-memory handle's) after the kernel
+    publishes the writes.
 """
 from __future__ import annotations
 
@@ -24,6 +32,12 @@ def row_range(n_rows: int, world: int, rank: int) -> tuple[int, int, int]:
     return r0, r1, blk
 
 
+def out_dtype(A):
+    """Result dtype of the C ABI: int64 (exact) for int32 coordinates, else float32."""
+    import torch
+    return torch.int64 if A.dtype == torch.int32 else torch.float32
+
+
 def assemble(block, n_rows: int, group=None):
     """All-gather equal-height row blocks [blk, nB] of every rank into [n_rows, nB]."""
     import torch
@@ -36,41 +50,67 @@ def assemble(block, n_rows: int, group=None):
     return full[:n_rows]
 
 
-def cdist(A, B, norm: str = "l2", group=None, return_block: bool = False):
+def _check_distribution(distribution: str):
+    if distribution not in ("allgather", "p2p"):
+        raise ValueError(f"distribution must be 'allgather' or 'p2p', got {distribution!r}")
+
+
+def symmetric_matrix(shape, dtype, device, group=None):
+    """A matrix in torch symmetric memory (every rank's copy mapped into every
+    rank's address space over NVLink).  Returns (tensor, handle, peer pointers in
+    rank order)."""
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm_mem
+
+    t = symm_mem.empty(*shape, dtype=dtype, device=device)
+    pg = group if group is not None else dist.group.WORLD
+    hdl = symm_mem.rendezvous(t, pg)
+    ptrs = [int(hdl.buffer_ptrs[r]) for r in range(hdl.world_size)]
+    return t, hdl, ptrs
+
+
+def cdist(A, B, norm: str = "l2", group=None, return_block: bool = False, distribution: str = "p2p"):
     """All-pairs δ_dF over the ranks of `group` (or the single local GPU).
 
     A [nA, lenA, dim], B [nB, lenB, dim] CUDA tensors, identical on every rank.
-    Returns the full [nA, nB] matrix on every rank (or only this rank's block
-    with return_block=True, skipping the collective)."""
-    import torch
+    Returns the full [nA, nB] matrix on every rank (float32, int64 for int32
+    input), or only this rank's block with return_block=True (no distribution)."""
     import torch.distributed as dist
 
     import paper_2404_05708_b200 as ffd
 
+    _check_distribution(distribution)
     nA, nB = A.shape[0], B.shape[0]
     if group is None and not (dist.is_available() and dist.is_initialized()):
         return ffd.cdist(A, B, norm=norm)
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     r0, r1, blk = row_range(nA, world, rank)
-    block = torch.empty((blk, nB), dtype=torch.int64 if A.dtype == torch.int32 else torch.float32,
-                        device=A.device)
+    if return_block or distribution == "allgather":
+        import torch
+        block = torch.empty((blk, nB), dtype=out_dtype(A), device=A.device)
+        if r1 > r0:
+            ffd.cdist(A, B, norm=norm, rows=(r0, r1), out=block)
+        if return_block:
+            return block[: r1 - r0], (r0, r1)
+        return assemble(block, nA, group)
+    full, hdl, ptrs = symmetric_matrix((nA, nB), out_dtype(A), A.device, group)
+    hdl.barrier()  # every rank's matrix is allocated before any peer writes into it
     if r1 > r0:
-        ffd.cdist(A, B, norm=norm, rows=(r0, r1), out=block)
-    if return_block:
-        return block[: r1 - r0], (r0, r1)
-    return assemble(block, nA, group)
+        ffd.cdist_to(A, B, ptrs, nB, norm=norm, rows=(r0, r1))
+    hdl.barrier()  # device-side: every rank's kernel (and its peer stores) is done
+    return full
 
 
 # ---------------------------------------------------------------------------
 # Self all-pairs matrix on W GPUs (SURVEY §8(f) f3).  δ is symmetric (PAPER L53),
-# so only the upper triangle b ≥ a is evaluated.  Rank r owns the rows
-# [r0, r1) and computes their columns [r0, n): its diagonal block with
-# ffd_cdist_self (each unordered pair once) and the block right of it with
-# ffd_cdist.  Row boundaries balance the upper-triangle work Σ_a (n − a) across
-# ranks; blocks are padded to one height H so that a single all_gather suffices;
-# the lower triangle is then the transpose of the upper one (selection only:
-# bit-identical to the single-GPU matrix).
+# so only the upper triangle b ≥ a is evaluated.  Rank r owns the rows [r0, r1)
+# and computes their columns [r0, n): its diagonal block as a self block (each
+# unordered pair once) and the block right of it as a plain block.  Row
+# boundaries balance the upper-triangle work Σ_a (n − a) across ranks.  The lower
+# triangle is the transpose of the upper one (selection only: bit-identical to
+# the single-GPU matrix): written as mirrored stores (p2p), or rebuilt from the
+# gathered upper-triangle rows (allgather, blocks padded to one height H).
 # ---------------------------------------------------------------------------
 def self_row_ranges(n: int, world: int) -> list[tuple[int, int]]:
     """Row shards [r0, r1) of the upper-triangle work, one per rank (contiguous,
@@ -90,9 +130,22 @@ def self_row_ranges(n: int, world: int) -> list[tuple[int, int]]:
     return [(bounds[r], bounds[r + 1]) for r in range(world)]
 
 
+def upper_from_gathered(full, n: int, ranges):
+    """The [n, n] matrix from gathered padded row blocks [W·H, n] that hold the
+    upper-triangle rows of every rank (columns < r0 ignored): its upper triangle,
+    mirrored."""
+    import torch
+
+    H = full.shape[0] // len(ranges)
+    rows = torch.cat([torch.arange(r * H, r * H + (r1 - r0), device=full.device)
+                      for r, (r0, r1) in enumerate(ranges)])
+    upper = torch.triu(full[rows])
+    return upper + torch.triu(upper, diagonal=1).T
+
+
 def assemble_upper(block, n: int, ranges, group=None):
     """All-gather padded row blocks [H, n] holding the upper-triangle rows of every
-    rank (columns < r0 are zero) and mirror them into the full [n, n] matrix."""
+    rank and mirror them into the full [n, n] matrix."""
     import torch
     import torch.distributed as dist
 
@@ -100,13 +153,27 @@ def assemble_upper(block, n: int, ranges, group=None):
     H, _ = block.shape
     full = torch.empty((world * H, n), dtype=block.dtype, device=block.device)
     dist.all_gather_into_tensor(full, block.contiguous(), group=group)
-    rows = torch.cat([torch.arange(r * H, r * H + (r1 - r0), device=block.device)
-                      for r, (r0, r1) in enumerate(ranges)])
-    upper = torch.triu(full[rows])
-    return upper + torch.triu(upper, diagonal=1).T
+    return upper_from_gathered(full, n, ranges)
 
 
-def cdist_self(A, norm: str = "l2", group=None):
+def self_block(A, r0: int, r1: int, norm: str = "l2"):
+    """Rank-local upper-triangle rows [r0, r1) of the self matrix, as an [r1 − r0, n]
+    block (columns < r0 zero): the diagonal block by ffd_cdist_self, the block to
+    its right by ffd_cdist."""
+    import torch
+
+    import paper_2404_05708_b200 as ffd
+
+    n = A.shape[0]
+    block = torch.zeros((r1 - r0, n), dtype=out_dtype(A), device=A.device)
+    if r1 > r0:
+        block[:, r0:r1] = ffd.cdist_self(A[r0:r1].contiguous(), norm=norm)
+        if r1 < n:
+            block[:, r1:] = ffd.cdist(A[r0:r1].contiguous(), A[r1:].contiguous(), norm=norm)
+    return block
+
+
+def cdist_self(A, norm: str = "l2", group=None, distribution: str = "p2p"):
     """All-pairs δ_dF of the set A against itself over the ranks of `group` (or the
     single local GPU): about half the work of cdist(A, A)."""
     import torch
@@ -114,17 +181,26 @@ def cdist_self(A, norm: str = "l2", group=None):
 
     import paper_2404_05708_b200 as ffd
 
+    _check_distribution(distribution)
     n = A.shape[0]
     if group is None and not (dist.is_available() and dist.is_initialized()):
         return ffd.cdist_self(A, norm=norm)
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     ranges = self_row_ranges(n, world)
-    H = max(1, max(r1 - r0 for r0, r1 in ranges))
     r0, r1 = ranges[rank]
-    block = torch.zeros((H, n), dtype=torch.float32, device=A.device)
+    if distribution == "allgather":
+        H = max(1, max(b - a for a, b in ranges))
+        block = torch.zeros((H, n), dtype=out_dtype(A), device=A.device)
+        block[: r1 - r0] = self_block(A, r0, r1, norm)
+        return assemble_upper(block, n, ranges, group)
+    full, hdl, ptrs = symmetric_matrix((n, n), out_dtype(A), A.device, group)
+    hdl.barrier()
+    A = A.contiguous()
     if r1 > r0:
-        block[: r1 - r0, r0:r1] = ffd.cdist_self(A[r0:r1].contiguous(), norm=norm)
-        if r1 < n:
-            block[: r1 - r0, r1:] = ffd.cdist(A[r0:r1].contiguous(), A[r1:].contiguous(), norm=norm)
-    return assemble_upper(block, n, ranges, group)
+        # diagonal block: each unordered pair inside the shard once, both places
+        ffd.cdist_to(A, A[r0:r1], ptrs, n, norm=norm, rows=(r0, r1), self_mode=True, col_offset=r0)
+        if r1 < n:  # right of it: (a, b) and its mirror (b, a)
+            ffd.cdist_to(A, A[r1:], ptrs, n, norm=norm, rows=(r0, r1), col_offset=r1, mirror=True)
+    hdl.barrier()
+    return full

@@ -119,7 +119,10 @@ def test_empty_pair_gets_nan(ffd):
     rng = np.random.default_rng(10)
     lens = np.array([5, 0, 6, 7, 3, 4], np.int32)
     b = make_batch(rng, 3, 0, 0, lens=lens)
-    out = ffd.batch(*to_dev(b), norm="l2").cpu().numpy()
+    with pytest.raises(ffd.FFDError) as e:     # the binding validates by default
+        ffd.batch(*to_dev(b), norm="l2")
+    assert e.value.status == -4
+    out = ffd.batch(*to_dev(b), norm="l2", validate=False).cpu().numpy()
     assert np.isnan(out[1])
     ok = [0, 2]
     for k in ok:
@@ -255,7 +258,7 @@ def test_prep_small_and_general_paths_agree(ffd, B):
     lens[5] = 0                       # empty: INT64_MIN
     lens[B + 7], lens[7] = 9000, 600  # long pair: the long-pair list
     b = make_batch(rng, B, 1, 300, kind="i", lens=lens)
-    got = ffd.batch(*to_dev(b), norm="sql2").cpu().numpy()
+    got = ffd.batch(*to_dev(b), norm="sql2", validate=False).cpu().numpy()
     ref = oracle.batch(b.p, b.q, b.offsets, b.lengths, b.dim, "sql2", check=False)
     assert got[5] == np.iinfo(np.int64).min
     keep = np.arange(B) != 5
@@ -326,3 +329,19 @@ def test_batch_host_pipelined_upload(ffd, layout):
     ref = oracle.batch(b.p, b.q, np.concatenate([off[sel], off[B + sel]]),
                        np.concatenate([lens[sel], lens[B + sel]]), b.dim, "sql2")
     assert np.array_equal(host[sel], ref)
+
+
+def test_strided_offsets_lengths_and_dim_check(ffd):
+    """The binding makes strided offsets/lengths contiguous and rejects
+    p/q of different dims before any launch."""
+    rng = np.random.default_rng(14)
+    b = make_batch(rng, 30, 1, 80)
+    p, q, off, lens = to_dev(b)
+    off2 = torch.stack([off, torch.full_like(off, 10**9)], 1).reshape(-1)[::2]   # stride 2
+    lens2 = torch.stack([lens, torch.zeros_like(lens)], 1).reshape(-1)[::2]
+    assert not off2.is_contiguous() and not lens2.is_contiguous()
+    got = ffd.batch(p, q, off2, lens2, norm="l2").cpu().numpy()
+    ref = ffd.batch(p, q, off, lens, norm="l2").cpu().numpy()
+    assert np.array_equal(got, ref)
+    with pytest.raises(ValueError):
+        ffd.batch(p, torch.zeros((5, 3), dtype=torch.float32, device="cuda"), off, lens)

@@ -495,6 +495,31 @@ def measure_cdist(args, cx, steps):
     launches = ffd.launches_taken() // steps
     ms_max, kern_max = cx.reduce([ms, kern_ms])
     checksum = float(full.double().sum().item())
+    # the fused distribution (dist.cdist(distribution="p2p")): every rank's kernel
+    # stores its results into all ranks' symmetric-memory matrices over NVLink,
+    # one device barrier publishes them — no gather in the step
+    p2p = None
+    if cx.ws > 1:
+        from paper_2404_05708_b200 import dist as fdist
+        try:
+            for _ in range(args.warmup):
+                fdist.cdist(A, B, cfg.norm, distribution="p2p")
+            torch.cuda.synchronize()
+            cx.barrier()
+            p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            p0.record(stream)
+            for _ in range(steps):
+                fp = fdist.cdist(A, B, cfg.norm, distribution="p2p")
+            p1.record(stream)
+            torch.cuda.synchronize()
+            p_ms = cx.reduce([p0.elapsed_time(p1) / steps])[0]
+            same = bool(torch.equal(fp, full))
+            p2p = {"value": total_cells / (p_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": p_ms,
+                   "matches_allgather_matrix": same,
+                   "api": "dist.cdist(distribution='p2p'): ffd_cdist_to into every rank's symmetric-memory "
+                          "matrix + one device barrier"}
+        except Exception as e:  # reported, never silently replaced
+            p2p = {"error": f"{type(e).__name__}: {e}"[:300]}
     # the gather alone (max over ranks): what the collective adds to the step
     gather_ms = None
     if cx.ws > 1:
@@ -543,6 +568,7 @@ def measure_cdist(args, cx, steps):
         "clocks": clocks,
         "kernel_ms_per_rank": kern_max,
         "all_gather_ms": gather_ms,
+        "p2p_distribution": p2p,
         "cpu_baseline": cpu_baseline_line(args, cfg, cx.ws),
         "roofline": roofline,
         "e2e": {"value": total_cells / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,

@@ -55,17 +55,27 @@ def _check_distribution(distribution: str):
         raise ValueError(f"distribution must be 'allgather' or 'p2p', got {distribution!r}")
 
 
+_SYMM_CACHE: dict = {}
+
+
 def symmetric_matrix(shape, dtype, device, group=None):
     """A matrix in torch symmetric memory (every rank's copy mapped into every
     rank's address space over NVLink).  Returns (tensor, handle, peer pointers in
-    rank order)."""
+    rank order).  Cached per (shape, dtype, device, group): the rendezvous is a
+    host-side exchange, done once; the next p2p call of the same shape reuses
+    (and overwrites) the buffer."""
     import torch.distributed as dist
     import torch.distributed._symmetric_memory as symm_mem
 
-    t = symm_mem.empty(*shape, dtype=dtype, device=device)
     pg = group if group is not None else dist.group.WORLD
+    key = (tuple(shape), dtype, str(device), id(pg))
+    hit = _SYMM_CACHE.get(key)
+    if hit is not None:
+        return hit
+    t = symm_mem.empty(*shape, dtype=dtype, device=device)
     hdl = symm_mem.rendezvous(t, pg)
     ptrs = [int(hdl.buffer_ptrs[r]) for r in range(hdl.world_size)]
+    _SYMM_CACHE[key] = (t, hdl, ptrs)
     return t, hdl, ptrs
 
 
@@ -74,7 +84,10 @@ def cdist(A, B, norm: str = "l2", group=None, return_block: bool = False, distri
 
     A [nA, lenA, dim], B [nB, lenB, dim] CUDA tensors, identical on every rank.
     Returns the full [nA, nB] matrix on every rank (float32, int64 for int32
-    input), or only this rank's block with return_block=True (no distribution)."""
+    input), or only this rank's block with return_block=True (no distribution).
+    distribution="p2p" returns the cached symmetric-memory matrix of this shape
+    (see symmetric_matrix): the next p2p call of the same shape overwrites it, so
+    clone it to keep it."""
     import torch.distributed as dist
 
     import paper_2404_05708_b200 as ffd

@@ -85,7 +85,7 @@ struct ProfScope {
   }
 };
 
-constexpr int kMaxCtasMain = 4;  // cap on resident CTAs/SM used to size scratch (= the 128-register occupancy)
+constexpr int kMaxCtasMain = kMinCtasPerSm > 4 ? kMinCtasPerSm : 4;  // cap on resident CTAs/SM used to size scratch
 constexpr int kCtasFb = 1;
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }

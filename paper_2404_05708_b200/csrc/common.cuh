@@ -29,10 +29,20 @@ constexpr int kRingMask = kRing - 1;
 constexpr int kChunkPairs = 8;      // pairs popped per scheduling chunk
 constexpr int kMaxR = 16;           // rows per lane, single warp band = 32*kMaxR rows
 constexpr int kMaxBands = 16;       // bands per pair in the batch kernel (rows ≤ 8192)
-constexpr int kScratchCols = 8256;  // bottom-stream capacity per warp for multi-band chunks
-                                    // (columns ≤ 8254: the paper's E2 sweep up to 2^13 stays here)
+constexpr int kScratchCols = 8260;  // bottom-stream capacity per warp for multi-band chunks
+                                    // (columns ≤ 8254: the paper's E2 sweep up to 2^13 stays here;
+                                    // the two-column layout needs m + 4 positions)
 constexpr int kWarpsPerCta = 4;
-constexpr int kMinCtasPerSm = 4;     // caps registers at 128/thread (16 warps/SM)
+#ifndef FFD_TWO_COL
+#define FFD_TWO_COL 0
+#endif
+// batch kernel: two columns per warp step (Fréchet).  Measured and off by default:
+// fewer fixed-latency waits, but the larger hot code thrashed the instruction cache.
+constexpr bool kTwoCol = FFD_TWO_COL != 0;
+#ifndef FFD_MIN_CTAS
+#define FFD_MIN_CTAS 4
+#endif
+constexpr int kMinCtasPerSm = FFD_MIN_CTAS;  // 4 caps registers at 128/thread (16 warps/SM)
 
 // fp32-exact integer window: translated coordinates |x| ≤ lim keep every value
 // of the K_XSQ / K_L1 / K_LINF evaluation an integer below 2^24 in magnitude.

@@ -15,7 +15,7 @@ constexpr int64_t kPrepSmallMax = 4096;      // batches up to this size: one-blo
 __host__ __device__ inline bool pair_too_long(int n, int m) {
   const int rows = n < m ? n : m, cols = n < m ? m : n;
   const int nb = (rows + kWarp * kMaxR - 1) / (kWarp * kMaxR);
-  return nb > kMaxBands || (nb > 1 && cols + 2 > kScratchCols);
+  return nb > kMaxBands || (nb > 1 && cols + 6 > kScratchCols);
 }
 
 // Fréchet pairs whose shorter curve needs 8 or more bands of 512 rows run on the

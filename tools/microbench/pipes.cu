@@ -12,6 +12,7 @@
 // Run:    ./pipes            (prints one JSON line per test)
 #include <cstdio>
 #include <cstdint>
+#include <cstring>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
@@ -188,17 +189,17 @@ __global__ void cell_kernel(float* out, long long* cyc, int steps) {
   const int lane = threadIdx.x & 31, w = (threadIdx.x >> 5) & 3;
   for (int i = lane; i < 128; i += 32)
     ring[w][i] = make_float4(i * 0.37f - 3.f, 1.5f - i * 0.21f, __int_as_float(i * 3 - 7), __int_as_float(5 - i));
-  float px[R], py[R], c[R];
+  float px[R], py[R], pq[R], c[R];
   int ipx[R], ipy[R], ipp[R], ic[R];
 #pragma unroll
   for (int r = 0; r < R; r++) {
-    px[r] = lane * 0.37f + r; py[r] = r * 0.11f - lane;
+    px[r] = lane * 0.37f + r; py[r] = r * 0.11f - lane; pq[r] = px[r] * px[r] + py[r] * py[r];
     c[r] = 1e30f;
     ipx[r] = lane * 3 + r; ipy[r] = r - lane; ipp[r] = ipx[r] * ipx[r] + ipy[r] * ipy[r];
     ic[r] = 0x7fffffff;
   }
-  float up_f = 0.f, diag_f = 0.f;
-  int up_i = 0, diag_i = 0;
+  float b0_f = 0.f, diag_f = 0.f;
+  int diag_i = 0;
   __syncthreads();
   long long t0 = clock64();
   int g = lane;
@@ -251,6 +252,78 @@ __global__ void cell_kernel(float* out, long long* cyc, int steps) {
         int nv = max(m, d);
         dg = ic[r]; ic[r] = nv; up = nv;
       }
+    } else if (VAR == 4 || VAR == 5 || VAR == 6) {
+      // the c2 cell: int input in fp32-exact arithmetic, d = (pp + qq) + p'·(−2q')
+      // on two rows at once (FADD2 + 2 FFMA2); VAR 4: chain FMNMX3 + FMNMX per row;
+      // VAR 5: m = min(diag, left) off the chain, chain FMNMX + FMNMX (ptxas may fuse);
+      // VAR 6: as 5 with m by an integer min on the (non-negative) float bits, which
+      // ptxas cannot fuse into the chain's FMNMX
+      float upv = SHF ? __shfl_up_sync(0xffffffffu, c[R - 1], 1) : c[R - 1];
+      float up = lane == 0 ? e.w : upv, dg = diag_f;
+      diag_f = up;
+      const uint64_t q2x = pack(e.x, e.x), q2y = pack(e.y, e.y), qq2 = pack(e.z, e.z);
+      float m[R];
+      if (VAR != 4) {
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+          const float left = c[r], above = r ? c[r - 1] : dg;
+          if (VAR == 6) m[r] = __int_as_float(min(__float_as_int(above), __float_as_int(left)));
+          else m[r] = fminf(above, left);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < R; r += 2) {
+        uint64_t acc;
+        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc) : "l"(pack(pq[r], pq[r + 1])), "l"(qq2));
+        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(pack(px[r], px[r + 1])), "l"(q2x));
+        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(pack(py[r], py[r + 1])), "l"(q2y));
+        const float d0 = __uint_as_float((uint32_t)acc), d1 = __uint_as_float((uint32_t)(acc >> 32));
+        float n0, n1;
+        if (VAR == 4) {
+          n0 = fmaxf(fminf(fminf(up, dg), c[r]), d0);
+          n1 = fmaxf(fminf(fminf(n0, c[r]), c[r + 1]), d1);
+        } else {
+          n0 = fmaxf(fminf(up, m[r]), d0);
+          n1 = fmaxf(fminf(n0, m[r + 1]), d1);
+        }
+        dg = c[r + 1]; c[r] = n0; c[r + 1] = n1; up = n1;
+      }
+    } else if (VAR == 7) {
+      // the c2 cell, TWO columns per step (strip.cuh Pipe2 layout): the second
+      // column's chain trails the first by one row, so the two chains interleave
+      const float4 e1 = ring[w][(g + 64) & 127];
+      const float upv0 = SHF ? __shfl_up_sync(0xffffffffu, b0_f, 1) : b0_f;
+      const float upv1 = SHF ? __shfl_up_sync(0xffffffffu, c[R - 1], 1) : c[R - 1];
+      const float up0 = lane == 0 ? e.w : upv0, up1 = lane == 0 ? e1.w : upv1;
+      float dist0[R], dist1[R];
+      const uint64_t q2x = pack(e.x, e.x), q2y = pack(e.y, e.y), qq2 = pack(e.z, e.z);
+      const uint64_t r2x = pack(e1.x, e1.x), r2y = pack(e1.y, e1.y), rq2 = pack(e1.z, e1.z);
+#pragma unroll
+      for (int r = 0; r < R; r += 2) {
+        uint64_t acc, acc1;
+        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc) : "l"(pack(pq[r], pq[r + 1])), "l"(qq2));
+        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(pack(px[r], px[r + 1])), "l"(q2x));
+        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(pack(py[r], py[r + 1])), "l"(q2y));
+        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc1) : "l"(pack(pq[r], pq[r + 1])), "l"(rq2));
+        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc1) : "l"(pack(px[r], px[r + 1])), "l"(r2x));
+        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc1) : "l"(pack(py[r], py[r + 1])), "l"(r2y));
+        dist0[r] = __uint_as_float((uint32_t)acc); dist0[r + 1] = __uint_as_float((uint32_t)(acc >> 32));
+        dist1[r] = __uint_as_float((uint32_t)acc1); dist1[r + 1] = __uint_as_float((uint32_t)(acc1 >> 32));
+      }
+      float u = up0, dg = diag_f;
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        const float nv = fmaxf(fminf(fminf(u, dg), c[r]), dist0[r]);
+        dg = c[r]; c[r] = nv; u = nv;
+      }
+      b0_f = c[R - 1];
+      u = up1; dg = up0;
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        const float nv = fmaxf(fminf(fminf(u, dg), c[r]), dist1[r]);
+        dg = c[r]; c[r] = nv; u = nv;
+      }
+      diag_f = up1;
     } else {
       int m2x = __float_as_int(e.x), m2y = __float_as_int(e.y), qq = __float_as_int(e.z);
       int upv = SHF ? __shfl_up_sync(0xffffffffu, ic[R - 1], 1) : ic[R - 1];
@@ -275,9 +348,12 @@ __global__ void cell_kernel(float* out, long long* cyc, int steps) {
 
 static int nsm;
 
+static const char* g_only = nullptr;  // argv[1]: run only the tests whose name contains it
+
 template <typename K>
 static int run(const char* name, K kern, int blocks_per_sm, int threads, int iters,
                double instr_per_thread_iter, const char* unit) {
+  if (g_only && !strstr(name, g_only)) return 0;
   int blocks = nsm * blocks_per_sm;
   float* out; long long* cyc;
   CK(cudaMalloc(&out, sizeof(float) * blocks * threads));
@@ -305,7 +381,8 @@ static int run(const char* name, K kern, int blocks_per_sm, int threads, int ite
   return 0;
 }
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1) g_only = argv[1];
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   cudaDeviceProp prop; cudaGetDeviceProperties(&prop, 0);
   printf("{\"device\": \"%s\", \"sms\": %d, \"cc\": \"%d.%d\"}\n", prop.name, nsm, prop.major, prop.minor);
@@ -350,6 +427,8 @@ int main() {
   for (int wi = 0; wi < 3; wi++) {
     int bps = wl[wi] / 4;  // 128-thread blocks
     char nm[96];
+#define CELL2(V, RR, S, TAG) snprintf(nm, 96, "cell_%s_R%d_shfl%d_w%d", TAG, RR, S, wl[wi]); \
+    run(nm, cell_kernel<V, RR, S>, bps, 128, ST, 2 * RR * 32.0, "cells");
 #define CELL(V, RR, S, TAG) snprintf(nm, 96, "cell_%s_R%d_shfl%d_w%d", TAG, RR, S, wl[wi]); \
     run(nm, cell_kernel<V, RR, S>, bps, 128, ST, RR * 32.0, "cells");
     CELL(0, 16, 0, "f32_scalar") CELL(0, 16, 1, "f32_scalar") CELL(0, 8, 1, "f32_scalar")
@@ -357,6 +436,10 @@ int main() {
     CELL(2, 16, 0, "i32_std") CELL(2, 16, 1, "i32_std") CELL(2, 8, 1, "i32_std")
     CELL(3, 16, 0, "i32_expand") CELL(3, 16, 1, "i32_expand") CELL(3, 8, 1, "i32_expand")
     CELL(3, 4, 1, "i32_expand") CELL(0, 4, 1, "f32_scalar")
+    CELL(4, 12, 1, "xsq_fmnmx3") CELL(5, 12, 1, "xsq_split") CELL(6, 12, 1, "xsq_split_int")
+    CELL(4, 16, 1, "xsq_fmnmx3") CELL(5, 16, 1, "xsq_split") CELL(6, 16, 1, "xsq_split_int")
+    CELL(4, 8, 1, "xsq_fmnmx3") CELL(5, 8, 1, "xsq_split") CELL(6, 8, 1, "xsq_split_int")
+    CELL2(7, 12, 1, "xsq_2col") CELL2(7, 16, 1, "xsq_2col") CELL2(7, 8, 1, "xsq_2col")
   }
   return 0;
 }

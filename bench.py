@@ -40,19 +40,24 @@ import workload  # noqa: E402
 METRIC = "DP cells/sec (G cells/s) batched & all-pairs Fréchet; % of ALU roofline"
 UNIT = "Gcells/s"
 SM_MAX_MHZ_NOMINAL = 1965.0
-# ALU roofline: peak cells/s = SMs × f_max × C, where C (cells per clock per SM) is
-# the MEASURED throughput of the cell's minimal SASS instruction mix run as independent chains at
-# 32 warps/SM (tools/microbench/pipes.cu `mixcells_*`, profiles/r1_microbench_pipes_v2.jsonl).  The
-# FMA pipe (FADD2/FFMA2/FMUL2) and the ALU pipe (FMNMX3/FMNMX) overlap, so this is above a
-# one-pipe count.  ISSUE_PER_CELL is the instruction count of that mix per warp-cell-row (issue
-# bound: 4 SMSPs × 1 instr/clk), reported beside it as the looser ceiling.
-MIX_CELLS_PER_CLK = {"f32_d2_sq": 29.683, "xsq_d2": 24.909, "f32_d3_sq": 16.592,
-                     "f32_d2_l1": 25.966, "f32_d2_linf": 22.754}
-ISSUE_PER_CELL = {"f32_d2_sq": 4.0, "xsq_d2": 3.5, "f32_d3_sq": 5.0, "f32_d2_l1": 4.0,
-                  "f32_d2_linf": 3.0}
+# ALU roofline (profiles/r2_pipe_model.md): peak cells/s = SMs × 4 SMSPs × 32 lanes ×
+# f_SM / (cycles per warp-cell on one SMSP), the cycles being the largest of the cell's ALU-pipe cycles,
+# FMA-pipe cycles and issue slots, with the per-instruction pipe costs MEASURED by ncu
+# (sm__pipe_alu_cycles_active / sm__pipe_fma_cycles_active of tools/microbench/pipes.cu): FMNMX and FMNMX3
+# keep the ALU pipe 2 cycles, FADD2/FMUL2/FFMA2 the FMA pipe 2 cycles, FADD 1.  Every Fréchet cell needs
+# min-of-three + max = 4 ALU cycles.
+#            cell: (ALU cycles, FMA cycles, issue slots) per warp-cell
+PIPE_MODEL = {"xsq_d2": (4, 3, 3.5), "f32_d2_sq": (4, 4, 4), "f32_d3_sq": (4, 6, 5),
+              "f32_d2_l1": (4, 3, 4), "f32_d2_linf": (4, 2, 3)}
+PEAK_SOURCE = "profiles/r2_pipe_model.md (ncu pipe counters of tools/microbench/pipes.cu)"
+
+
+def cells_per_clk_per_sm(cell):
+    return 4 * 32 / max(PIPE_MODEL[cell])
+
+
 CELL_OF_CONFIG = {1: "f32_d2_sq", 2: "xsq_d2", 3: "f32_d3_sq", 4: "f32_d2_sq", 5: "f32_d2_sq"}
 CELL_OF_NORM = {"l1": "f32_d2_l1", "l2": "f32_d2_sq", "linf": "f32_d2_linf"}
-MIX_SOURCE = "profiles/r1_microbench_pipes_v2.jsonl (tools/microbench/pipes.cu mixcells_*)"
 # roofline.traffic (dram bytes per launch of the dominant kernel) is not measurable inside a plain
 # run; it is null here, and the ncu --set full captures of the same kernels, with their dram
 # bytes against the algorithmic bytes, are committed under profiles/ (named per round).
@@ -80,15 +85,14 @@ def timed_steps_flushed(torch, stream, dev, fn, steps):
 def alu_roofline(cells_per_launch, kernel_ms, cell, sms, f_max, f_meas, kernel, traffic):
     """The roofline object for the dominant kernel."""
     achieved = cells_per_launch / (kernel_ms * 1e-3) / 1e9
-    c = MIX_CELLS_PER_CLK[cell]
+    c = cells_per_clk_per_sm(cell)
+    alu, fma, issue = PIPE_MODEL[cell]
     peak = sms * c * f_max / 1e9
-    issue_peak = sms * 128.0 / ISSUE_PER_CELL[cell] * f_max / 1e9
     return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": UNIT, "frac": achieved / peak,
             "traffic": traffic, "kernel": kernel, "kernel_ms": kernel_ms, "cell": cell,
-            "peak_basis": f"{sms} SMs x {c} cells/clk/SM (measured mix of the cell's SASS ops, {MIX_SOURCE})"
-                          f" x {f_max/1e6:.0f} MHz (max SM clock)",
-            "frac_at_measured_clock": achieved / (sms * c * f_meas / 1e9),
-            "issue_bound_peak": issue_peak, "frac_of_issue_bound": achieved / issue_peak}
+            "peak_basis": f"{sms} SMs x 128 lanes / max(ALU {alu}, FMA {fma}, issue {issue}) cycles per warp-cell "
+                          f"= {c:.2f} cells/clk/SM x {f_max/1e6:.0f} MHz (max SM clock); {PEAK_SOURCE}",
+            "frac_at_measured_clock": achieved / (sms * c * f_meas / 1e9)}
 
 
 def dist_env():

@@ -67,9 +67,20 @@ constexpr int kLSmemRing = 1024;    // slots per intra-CTA link (8 KB; the produ
                                     // ~500 steps ahead, far beyond the ~47 the consumer needs)
 constexpr int kLGlobRing = 2048;    // slots per inter-CTA link
 constexpr int kMaxLongCtas = 1024;
+#ifndef FFD_LONG_COLS
+#define FFD_LONG_COLS 2
+#endif
+// columns per warp step of the fp32 tier (2 or 4).  Four halve the steps per column but measured
+// slower on config 5 (39.5 against 33 ms per norm: the step time doubled), so two stay the default.
+constexpr int kLCols = FFD_LONG_COLS;
+#ifndef FFD_LONG_R16
+#define FFD_LONG_R16 1
+#endif
+constexpr bool kLR16 = FFD_LONG_R16 != 0;  // build the R = 16 bands (fp32 tier)
 // a spin on a link that has not advanced for this many SM cycles (≈ 2.5 s)
 // reports the link state with printf, sets the abort flag and gives up
 constexpr long long kWatchdogCycles = 5000000000LL;
+constexpr long long kAbortCheckCycles = 1LL << 20;  // spins read the abort flag only after ~0.5 ms
 
 struct LongProblem {
   const void* p;
@@ -87,6 +98,7 @@ struct LongProblem {
   int* bad;        // per long pair: a point left the fp32-exact window (int input, fp32 tier)
   int* abort;      // a watchdog fired: every spin gives up, results become NaN / INT64_MIN
   int trace;       // FFD_LONG_TRACE=1: print each band's start/end time
+  int force_r;     // FFD_LONG_R (testing): rows per lane instead of the automatic choice
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -178,6 +190,83 @@ struct Link {
   unsigned* cons;
 };
 
+constexpr int kLRing = 256;  // column-ring positions per warp: lane 31 trails lane 0 by 31·K ≤ 124
+constexpr int kLRingMask = kLRing - 1;
+// ring slot of stream position p with K columns per step: lane ℓ reads positions
+// K(t−ℓ)+k, so consecutive lanes would be K·16 B apart (a 2K-way shared-memory
+// bank conflict on every element load); grouping the slots by p mod K makes
+// their reads consecutive (conflict-free)
+template <int K>
+__device__ __forceinline__ int lring(int p) {
+  return (p & (K - 1)) * (kLRing / K) + ((p / K) & (kLRing / K - 1));
+}
+
+// K columns per warp step (K = 2 or 4): lane ℓ at step t works on positions
+// K(t−ℓ) … K(t−ℓ)+K−1.  Column k's chain trails column k−1's by one row (cell
+// (r, k) needs (r, k−1) and (r−1, k)), so the K chains interleave and the
+// shuffle + chain latency is paid once per K columns.  Lane ℓ hands lane ℓ+1 its
+// bottom value after each of the K columns (K shuffles per step).  Software-
+// pipelined like strip.cuh Pipe2: the distances of step g+1 are computed during
+// step g's chains and the ring elements of step g+2 are loaded.
+template <typename T, int KIND, int D, int R, bool INT_IN, int K>
+struct PipeK {
+  using C = SCfg<T, KIND, D, INT_IN>;
+  static constexpr int N = C::EBYTES / sizeof(T);
+  T d[K][R];   // distances of the step to execute next
+  T top[K];    // its top values (lane 0)
+  alignas(16) T nxt[K][N];  // the elements of the step after it
+
+  __device__ __forceinline__ void load(T (&el)[K][N], const uint4* __restrict__ ring, int g) const {
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+      const uint4* src = ring + lring<K>(K * g + k) * C::EW;
+#pragma unroll
+      for (int w = 0; w < C::EW; w++) reinterpret_cast<uint4*>(el[k])[w] = src[w];
+    }
+  }
+
+  __device__ __forceinline__ void prime(const T (&x)[C::NS][R], const uint4* __restrict__ ring, int g) {
+    alignas(16) T el[K][N];
+    load(el, ring, g);
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+      cell_dists<T, KIND, D, R, INT_IN>(x, el[k], d[k]);
+      top[k] = el[k][C::I_TOP];
+    }
+    load(nxt, ring, g + 1);
+  }
+
+  __device__ __forceinline__ void step(T (&c)[R], T& diag, T (&b)[K], const T (&x)[C::NS][R],
+                                       const uint4* __restrict__ ring, int g, int lane) {
+    T up[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+      const T upv = __shfl_up_sync(0xffffffffu, b[k], 1);
+      up[k] = (lane == 0) ? top[k] : upv;
+    }
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+      T u = up[k], dg = (k == 0) ? diag : up[k - 1];
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        const T m = tmin(tmin(u, dg), c[r]);
+        const T nv = tmax(m, d[k][r]);
+        dg = c[r];
+        c[r] = nv;
+        u = nv;
+      }
+      b[k] = c[R - 1];
+    }
+    diag = up[K - 1];
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+      cell_dists<T, KIND, D, R, INT_IN>(x, nxt[k], d[k]);
+      top[k] = nxt[k][C::I_TOP];
+    }
+    load(nxt, ring, g + 2);
+  }
+};
+
 template <typename T, int KIND, int D, bool INT_IN, int FIN, int R>
 struct LongRunner {
   using C = SCfg<T, KIND, D, INT_IN>;
@@ -186,7 +275,7 @@ struct LongRunner {
   using In = typename std::conditional<INT_IN, int32_t, float>::type;
   static constexpr int NS = C::NS;
 
-  uint4* ring;  // this warp's column ring [kRing * EW]
+  uint4* ring;  // this warp's column ring [kLRing * EW]
   const LongProblem& pb;
   int lane;
 
@@ -214,6 +303,7 @@ struct LongRunner {
   }
 
   // column element of position `pos` (0 = sentinel), written with its top value
+  template <int K>
   __device__ void store_elem(const In (&a)[D], int kind, int pos, T top, bool& ok) {
     alignas(16) T f[C::EBYTES / sizeof(T)];
 #pragma unroll
@@ -244,14 +334,14 @@ struct LongRunner {
       }
     }
     f[C::I_TOP] = top;
-    uint4* dst = ring + (pos & kRingMask) * C::EW;
+    uint4* dst = ring + lring<K>(pos) * C::EW;
 #pragma unroll
     for (int w = 0; w < C::EW; w++) dst[w] = reinterpret_cast<const uint4*>(f)[w];
   }
 
-  // positions: 0 = sentinel, p ∈ [1, m] = column p − 1, and when m + 1 is odd one
-  // more copy of the last column (repeating a point leaves δ unchanged, PAPER
-  // L259 footnote) so the stream has an even length S2 (two columns per step)
+  // positions: 0 = sentinel, p ∈ [1, m] = column p − 1, and up to K − 1 more
+  // copies of the last column (repeating a point leaves δ unchanged, PAPER L259
+  // footnote) so that the stream length S2 is a multiple of K (K columns per step)
   __device__ void fetch(int pos, int S2, In (&a)[D], int& kind) const {
 #pragma unroll
     for (int c = 0; c < D; c++) a[c] = (In)0;
@@ -278,7 +368,8 @@ struct LongRunner {
       const long long t0 = clock64();
       while (!SL::ready(pre, want)) {
         pre = SL::load(in.ring, in.mask, tb + (unsigned)pos);
-        if (aborted(pb.abort)) break;
+        // the abort flag is an L2 round trip: read it only in a long wait
+        if (clock64() - t0 > kAbortCheckCycles && aborted(pb.abort)) break;
         if (clock64() - t0 > kWatchdogCycles) {  // a link that never delivers: report, abort
           printf("ffd long_kernel watchdog: consumer cta %d lane %d pos %d want tag %u (tb %u)\n",
                  (int)blockIdx.x, lane, pos, want, tb);
@@ -304,7 +395,7 @@ struct LongRunner {
         const long long t0 = clock64();
         while (!SL::ready(SL::load(in.ring, in.mask, tb + (unsigned)pos), want)) {
           __nanosleep(64);
-          if (aborted(pb.abort)) break;
+          if (clock64() - t0 > kAbortCheckCycles && aborted(pb.abort)) break;
           if (clock64() - t0 > kWatchdogCycles) {
             printf("ffd long_kernel watchdog: chunk wait cta %d pos %d want tag %u (tb %u)\n",
                    (int)blockIdx.x, pos, want, tb);
@@ -317,13 +408,15 @@ struct LongRunner {
     __syncwarp();
   }
 
-  // one band of 32·R rows starting at row r0, two columns per warp step
-  // (strip.cuh Pipe2: lane ℓ at step t works on columns 2(t−ℓ), 2(t−ℓ)+1).
+  // one band of 32·R rows starting at row r0, K columns per warp step (PipeK).
   // tbi / tbo: tag bases of the input / output link streams.
+  template <int K>
   __device__ bool run_band(int r0, bool has_in, Link in, unsigned tbi, bool has_out, Link out,
                            unsigned tbo, bool last_band, int out_idx, int* bad_flag) {
-    const int S2 = (m + 2) & ~1;  // positions (even)
-    const int NT = S2 / 2;        // steps
+    static_assert(K == 2 || K == 4, "K columns per step");
+    constexpr int P = 32 / K;                  // steps per 32-position chunk
+    const int S2 = (m + 1 + K - 1) / K * K;    // positions (a multiple of K)
+    const int NT = S2 / K;                     // steps
     bool ok = true;
     T x[NS][R], c[R];
 #pragma unroll
@@ -347,16 +440,18 @@ struct LongRunner {
     if constexpr (INT_IN && C::F) {
       if (!__all_sync(0xffffffffu, ok) && lane == 0) atomicExch(bad_flag, 1);
     }
-    T diag = tinf<T>(), b0 = tinf<T>();
+    T diag = tinf<T>(), b[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) b[k] = tinf<T>();
     // prologue: positions [0, 32) stored; column points of [32, 64) and [64, 96)
-    // in flight (two chunks ahead: one 16-step chunk does not cover the L2/HBM
-    // latency of a latency-bound warp); link slots of [32, 64) in flight
+    // in flight (two chunks ahead: one chunk does not cover the L2/HBM latency of
+    // a latency-bound warp); link slots of [32, 64) in flight
     In a[D], a2[D];
     int kind, kind2;
     fetch(lane, S2, a, kind);
     wait_chunk(31, S2, has_in, in, tbi);
     Pre pre = (has_in && lane < S2) ? SL::load(in.ring, in.mask, tbi + (unsigned)lane) : SL::none();
-    store_elem(a, kind, lane, top_of(lane, S2, has_in, in, tbi, pre), ok);
+    store_elem<K>(a, kind, lane, top_of(lane, S2, has_in, in, tbi, pre), ok);
     fetch(32 + lane, S2, a, kind);
     fetch(64 + lane, S2, a2, kind2);
     pre = (has_in && 32 + lane < S2) ? SL::load(in.ring, in.mask, tbi + (unsigned)(32 + lane)) : SL::none();
@@ -368,40 +463,41 @@ struct LongRunner {
 
     const int total = NT + 31;
     const int pown = (has_out && lane == kWarp - 1) ? 1 : 0;
-    int t = 0, next_refill = 16;
+    int t = 0, next_refill = P;
     while (t < total) {
       if (t == next_refill) {
         // the slots of this chunk were prefetched one chunk ago: when every tag
         // is already there, go on without touching the link (a blocking poll of
         // an L2 link costs ~700 cycles per chunk); else wait on lane 0 first
-        if (2 * t < S2 && has_in) {
-          const int pos = 2 * t + lane;
+        const int p0 = K * t;
+        if (p0 < S2 && has_in) {
+          const int pos = p0 + lane;
           const bool ready = pos >= S2 || SL::ready(pre, tbi + (unsigned)pos + 1u);
-          if (!__all_sync(0xffffffffu, ready)) wait_chunk(2 * t + 31, S2, has_in, in, tbi);
+          if (!__all_sync(0xffffffffu, ready)) wait_chunk(p0 + 31, S2, has_in, in, tbi);
         }
-        store_elem(a, kind, 2 * t + lane, top_of(2 * t + lane, S2, has_in, in, tbi, pre), ok);
+        store_elem<K>(a, kind, p0 + lane, top_of(p0 + lane, S2, has_in, in, tbi, pre), ok);
 #pragma unroll
         for (int cc = 0; cc < D; cc++) a[cc] = a2[cc];
         kind = kind2;
-        fetch(2 * t + 64 + lane, S2, a2, kind2);
-        const int pn = 2 * t + 32 + lane;
+        fetch(p0 + 64 + lane, S2, a2, kind2);
+        const int pn = p0 + 32 + lane;
         pre = (has_in && pn < S2) ? SL::load(in.ring, in.mask, tbi + (unsigned)pn) : SL::none();
         __syncwarp();
-        if (has_in && lane == 0) st_ctr(in.cons, tbi + (unsigned)min(2 * t + 32, S2));
-        next_refill += 16;
+        if (has_in && lane == 0) st_ctr(in.cons, tbi + (unsigned)min(p0 + 32, S2));
+        next_refill += P;
       }
-      if (has_out && (t & 15) == 0) {
-        // lane 31 writes positions < 2t + 32 during the next 16 steps: their
-        // slots must be consumed (cons + capacity > tbo + 2t).  The counter is
-        // read a chunk ahead.
+      if (has_out && (t % P) == 0) {
+        // lane 31 writes positions < K·t during the next P steps: their slots
+        // must be consumed (cons + capacity > tbo + K·t).  The counter is read a
+        // chunk ahead.
         if (lane == kWarp - 1) {
           cons_seen = cons_next;
-          if ((int)(cons_seen + cap - (tbo + 2u * (unsigned)t)) <= 0) {
+          if ((int)(cons_seen + cap - (tbo + (unsigned)(K * t))) <= 0) {
             const long long t0 = clock64();
-            while ((int)(cons_seen + cap - (tbo + 2u * (unsigned)t)) <= 0) {
+            while ((int)(cons_seen + cap - (tbo + (unsigned)(K * t))) <= 0) {
               __nanosleep(64);
               cons_seen = ld_ctr(out.cons);
-              if (aborted(pb.abort)) break;
+              if (clock64() - t0 > kAbortCheckCycles && aborted(pb.abort)) break;
               if (clock64() - t0 > kWatchdogCycles) {
                 printf("ffd long_kernel watchdog: producer cta %d warp %d t %d cons %u tb %u cap %u\n",
                        (int)blockIdx.x, (int)(threadIdx.x >> 5), t, cons_seen, tbo, cap);
@@ -416,17 +512,17 @@ struct LongRunner {
       __syncwarp();
       const int stop = min(next_refill, total);
       int g = t - lane;
-      // software-pipelined steps (strip.cuh Pipe2): the distances of step g+1 are
-      // computed during step g's chain and the ring element of g+2 is loaded;
       // primed again after every refill (its look-ahead may read unstored slots)
-      Pipe2<T, KIND, D, R, INT_IN> pipe;
+      PipeK<T, KIND, D, R, INT_IN, K> pipe;
       pipe.prime(x, ring, g);
-      // lane 31 publishes its two bottom-row values {value, tag} of every step
-      // with one predicated store (no divergent branch per step)
+      // lane 31 publishes its K bottom-row values {value, tag} of every step with
+      // predicated 16-byte stores (no divergent branch per step)
       auto one = [&](int gg) {
-        pipe.step(c, diag, b0, x, ring, gg, lane);
-        SL::put2(out.ring, out.mask, tbo + 2u * (unsigned)gg, b0, c[R - 1],
-                 pown & ((unsigned)gg < (unsigned)NT));
+        pipe.step(c, diag, b, x, ring, gg, lane);
+        const int pr = pown & ((unsigned)gg < (unsigned)NT);
+#pragma unroll
+        for (int k = 0; k < K; k += 2)
+          SL::put2(out.ring, out.mask, tbo + (unsigned)(K * gg + k), b[k], b[k + 1], pr);
       };
 #pragma unroll 1
       for (; t + 2 <= stop; t += 2, g += 2) {
@@ -473,13 +569,13 @@ __host__ __device__ inline bool long_rows_fit(int n, int G, int& R) {
   const int rs_f[4] = {4, 7, 8, 16};  // the R the fp32 tier is built for
   const int rs_i[2] = {4, 8};         // the R the int64 tier is built for
   const int* rs = F ? rs_f : rs_i;
-  const int nr = F ? 4 : 2;
+  const int nr = F ? (kLR16 ? 4 : 3) : 2;
   for (int i = 0; i < nr; i++) {
     R = rs[i];
     const int nb = (n + kWarp * R - 1) / (kWarp * R);
     if ((nb + kLWarps - 1) / kLWarps <= G) return true;
   }
-  R = F ? 16 : 8;
+  R = F && kLR16 ? 16 : 8;
   return false;
 }
 
@@ -488,13 +584,13 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
   using C = SCfg<T, KIND, D, INT_IN>;
   using In = typename std::conditional<INT_IN, int32_t, float>::type;
   constexpr bool TIER64 = !C::F;  // int64 tier: only the pairs the fp32 tier flagged
-  // dynamic shared memory: [kLWarps][kLSmemRing] link slots, [kLWarps][kRing·EW]
+  // dynamic shared memory: [kLWarps][kLSmemRing] link slots, [kLWarps][kLRing·EW]
   // column rings, [kLWarps] consumer counters
   extern __shared__ uint4 lsm[];
   uint2 (*slink)[kLSmemRing] = reinterpret_cast<uint2(*)[kLSmemRing]>(lsm);
-  uint4 (*rings)[kRing * C::EW] =
-      reinterpret_cast<uint4(*)[kRing * C::EW]>(lsm + kLWarps * kLSmemRing / 2);
-  unsigned* scons = reinterpret_cast<unsigned*>(lsm + kLWarps * kLSmemRing / 2 + kLWarps * kRing * C::EW);
+  uint4 (*rings)[kLRing * C::EW] =
+      reinterpret_cast<uint4(*)[kLRing * C::EW]>(lsm + kLWarps * kLSmemRing / 2);
+  unsigned* scons = reinterpret_cast<unsigned*>(lsm + kLWarps * kLSmemRing / 2 + kLWarps * kLRing * C::EW);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x, cta = blockIdx.x;
   const int npairs = *pb.list_count;
@@ -543,13 +639,23 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
     const int k = pb.list[li];
     const int n0 = pb.lengths[k], m0 = pb.lengths[pb.num_pairs + k];
     const int rows = n0 < m0 ? n0 : m0;
-    constexpr int RN = C::F ? 16 : 8;  // the tallest band without spills
+    constexpr int RN = C::F && kLR16 ? 16 : 8;  // the tallest built band
     const int nbn = (rows + kWarp * RN - 1) / (kWarp * RN);
     need = max(need, (nbn + kLWarps - 1) / kLWarps);
   }
   need = min(need, G);
   const int NG = max(1, min(G / need, nsel));
   const int Gg = G / NG;
+  // rows per lane of a pair whose shorter curve has n points; false: multi-pass
+  auto choose_r = [&](int n, int& R) {
+    bool fit = long_rows_fit<T>(n, Gg, R);
+    if (pb.force_r && C::F && (pb.force_r == 4 || pb.force_r == 7 || pb.force_r == 8 || (kLR16 && pb.force_r == 16))) {
+      R = pb.force_r;  // testing: a built R; multi-pass if its bands do not fit at once
+      const int nbf = (n + kWarp * R - 1) / (kWarp * R);
+      fit = (nbf + kLWarps - 1) / kLWarps <= Gg;
+    }
+    return fit;
+  };
   // Multi-pass pairs (only possible with one group: every pair fits one pass on
   // a group of `need` CTAs) stream their SHORTER curve as columns through the
   // HBM wrap link, whose ring is sized once per launch to the longest such
@@ -560,7 +666,7 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
     const int k = pb.list[li];
     const int n0 = pb.lengths[k], m0 = pb.lengths[pb.num_pairs + k];
     int Rx;
-    if (long_rows_fit<T>(n0 < m0 ? n0 : m0, Gg, Rx)) continue;
+    if (choose_r(n0 < m0 ? n0 : m0, Rx)) continue;
     const unsigned long long need_slots =
         (unsigned long long)((min(n0, m0) + 2) & ~1) * Slots<T>::SPP;
     unsigned long long cap = 2;
@@ -616,7 +722,7 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
     int R;
     // one pass: the shorter curve on the rows; multi-pass: the longer one (the
     // wrap link then buffers the shorter curve's stream)
-    const bool multi = !long_rows_fit<T>(n0 < m0 ? n0 : m0, Gg, R);
+    const bool multi = !choose_r(n0 < m0 ? n0 : m0, R);
     const bool swap = multi ? n0 < m0 : n0 > m0;
     const int n = swap ? m0 : n0, m = swap ? n0 : m0;
     const In* rows = reinterpret_cast<const In*>(swap ? pb.q : pb.p) +
@@ -660,7 +766,9 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
             for (int c = 0; c < D; c++) run.center[c] = (int)rows[c];
           }
           const unsigned long long t0 = pb.trace ? gtimer() : 0ull;
-          run.run_band(b * band_rows, has_in, lin, tb, has_out, lout, tbo, b == nb - 1, k, pb.bad + li);
+          // fp32: four columns per step; int64 tier: two (its 64-bit state doubles the registers)
+          run.template run_band<TIER64 ? 2 : kLCols>(b * band_rows, has_in, lin, tb, has_out, lout, tbo,
+                                                     b == nb - 1, k, pb.bad + li);
           if (pb.trace && lane == 0)
             printf("ffdtrace band %d cta %d warp %d start %llu end %llu\n", b, cta, warp, t0, gtimer());
         };
@@ -682,7 +790,7 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
           } else if (R == 8) {
             LongRunner<T, KIND, D, INT_IN, FIN, 8> run{rings[warp], pb, lane};
             go(run);
-          } else {
+          } else if constexpr (kLR16) {
             LongRunner<T, KIND, D, INT_IN, FIN, 16> run{rings[warp], pb, lane};
             go(run);
           }
@@ -709,7 +817,7 @@ template <typename T, int KIND, int D, bool INT_IN, int FIN>
 cudaError_t launch_long_k(const LongArgs& a, int sms, cudaStream_t st, const LongWs& w, int G) {
   auto k = long_kernel<T, KIND, D, INT_IN, FIN>;
   using C = SCfg<T, KIND, D, INT_IN>;
-  const size_t smem = sizeof(uint2) * kLWarps * kLSmemRing + sizeof(uint4) * kLWarps * kRing * C::EW +
+  const size_t smem = sizeof(uint2) * kLWarps * kLSmemRing + sizeof(uint4) * kLWarps * kLRing * C::EW +
                       sizeof(unsigned) * kLWarps;
   // per-device caches: attribute, occupancy and the cluster shape for this grid
   // (the host-side queries would otherwise cost tens of µs on every call)
@@ -729,8 +837,10 @@ cudaError_t launch_long_k(const LongArgs& a, int sms, cudaStream_t st, const Lon
   unsigned wrap_slots = 0;  // the largest power of two of slots the wrap buffer holds
   for (unsigned long long c = 1; c * sizeof(uint2) <= a.wrap_bytes && c <= 0x80000000ull; c <<= 1)
     wrap_slots = (unsigned)c;
+  static const int force_r = getenv("FFD_LONG_R") ? atoi(getenv("FFD_LONG_R")) : 0;
   LongProblem pb{a.p,     a.q,     a.offsets, a.lengths,  a.num_pairs, a.list, a.list_count, a.out,
-                 w.gring, w.gcons, reinterpret_cast<uint2*>(a.wrap), wrap_slots, w.bad, w.abort, trace};
+                 w.gring, w.gcons, reinterpret_cast<uint2*>(a.wrap), wrap_slots, w.bad, w.abort, trace,
+                 force_r};
   void* args[] = {&pb};
   // cluster size: the largest of 8/4/2 whose clusters can all be co-resident
   // for the whole grid (a smaller grid forces taller bands); FFD_LONG_CLUSTER=c

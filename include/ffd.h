@@ -90,9 +90,10 @@ size_t ffd_batch_workspace_bytes(int64_t num_pairs);
  *   stream semantics as ffd_batch.  dtype must be FFD_F32 (FFD_ERR_UNSUPPORTED
  *   otherwise); FFD_L2 evaluates sqrt per cell; sums are accumulated in fp32 in
  *   the DP's own order (relative error ≤ (n+m+D+2)·2⁻²⁴ of the exact value).
- *   Pairs whose shorter curve needs more than 16 bands of 512 rows, or more
- *   than one band with the longer curve above 8254 points, get NaN (no
- *   long-pair path for DTW).                                                     */
+ *   Any lengths: pairs too long for the batch kernel's bands (more than 16
+ *   bands of 512 rows, or more than one band with the longer curve above 8254
+ *   points) run on the long-pair kernel with the DTW cell (the shorter curve
+ *   on the rows).                                                               */
 int ffd_batch_dtw(const void* p, const void* q, const int64_t* offsets, const int32_t* lengths,
                   int64_t num_pairs, int32_t dim, int32_t norm, int32_t dtype, void* out,
                   void* workspace, size_t workspace_bytes, ffd_stream_t stream);

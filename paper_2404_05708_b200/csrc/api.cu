@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <atomic>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -161,7 +162,10 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
     if (!fb_e) return FFD_ERR_UNSUPPORTED;
   }
 
-  const int long_ok = measure == 0 ? medium_rows_for(B, di.sms) : 0;
+  // Fréchet: pairs too long for the bands, and the medium ones, go to the long-pair
+  // kernel; DTW (−1): only those too long for the bands (its sums keep one orientation)
+  const bool dtw_all_long = measure == 1 && getenv("FFD_DTW_LONG") != nullptr;  // testing: every DTW pair long
+  const int long_ok = measure == 0 ? medium_rows_for(B, di.sms) : (dtw_all_long ? -2 : -1);
   if (launch_prep(offsets, lengths, B, int_in, long_ok, out, ws, di.sms, st, &g_launches) !=
       cudaSuccess)
     return FFD_ERR_CUDA;
@@ -216,7 +220,6 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
     ++g_launches;
   }
 
-  if (measure != 0) return FFD_OK;  // DTW: no long-pair path (prep wrote NaN for those pairs)
   if (!long_possible) return FFD_OK;  // the caller saw every length: no pair is long
   // pairs too long for the band scratch of the batch kernel: cross-CTA wavefront
   LongArgs la{};
@@ -228,6 +231,7 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
   la.dim = dim;
   la.norm = norm;
   la.dtype = dtype;
+  la.measure = measure;
   la.list = ws.long_list;
   la.list_count = ws.counters + kCtrLong;
   la.out = out;

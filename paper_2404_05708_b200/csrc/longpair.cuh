@@ -11,6 +11,7 @@ struct LongArgs {
   const int32_t* lengths;
   int64_t num_pairs;
   int dim, norm, dtype;
+  int measure;            // 0: discrete Fréchet (Eq. (1)); 1: DTW (PAPER Appendix B)
   const int* list;        // device list of long pair indices
   const int* list_count;  // device count
   void* out;

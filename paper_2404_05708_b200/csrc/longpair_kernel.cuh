@@ -192,6 +192,22 @@ struct Link {
 
 constexpr int kLRing = 256;  // column-ring positions per warp: lane 31 trails lane 0 by 31·K ≤ 124
 constexpr int kLRingMask = kLRing - 1;
+// A pair's column stream with K columns per step: `lead` sentinel positions
+// (1 … K) so that its length lead + m is a multiple of K, then the m columns.  A
+// second sentinel in front changes nothing (both reset every row to +∞); the
+// corner value 0 sits at position lead − 1.  Padding in front, not behind,
+// keeps the last column the last position, which DTW needs (a repeated column
+// would add to its sums).
+template <int K>
+__host__ __device__ inline int stream_lead(int m) {
+  const int r = m % K;
+  return r ? K - r : K;
+}
+template <int K>
+__host__ __device__ inline int stream_len(int m) {
+  return stream_lead<K>(m) + m;
+}
+
 // ring slot of stream position p with K columns per step: lane ℓ reads positions
 // K(t−ℓ)+k, so consecutive lanes would be K·16 B apart (a 2K-way shared-memory
 // bank conflict on every element load); grouping the slots by p mod K makes
@@ -208,7 +224,7 @@ __device__ __forceinline__ int lring(int p) {
 // bottom value after each of the K columns (K shuffles per step).  Software-
 // pipelined like strip.cuh Pipe2: the distances of step g+1 are computed during
 // step g's chains and the ring elements of step g+2 are loaded.
-template <typename T, int KIND, int D, int R, bool INT_IN, int K>
+template <typename T, int KIND, int D, int R, bool INT_IN, int K, bool DTW = false>
 struct PipeK {
   using C = SCfg<T, KIND, D, INT_IN>;
   static constexpr int N = C::EBYTES / sizeof(T);
@@ -250,7 +266,9 @@ struct PipeK {
 #pragma unroll
       for (int r = 0; r < R; r++) {
         const T m = tmin(tmin(u, dg), c[r]);
-        const T nv = tmax(m, d[k][r]);
+        T nv;
+        if constexpr (DTW) nv = m + d[k][r];  // PAPER Appendix B: min3 + d
+        else nv = tmax(m, d[k][r]);
         dg = c[r];
         c[r] = nv;
         u = nv;
@@ -339,19 +357,17 @@ struct LongRunner {
     for (int w = 0; w < C::EW; w++) dst[w] = reinterpret_cast<const uint4*>(f)[w];
   }
 
-  // positions: 0 = sentinel, p ∈ [1, m] = column p − 1, and up to K − 1 more
-  // copies of the last column (repeating a point leaves δ unchanged, PAPER L259
-  // footnote) so that the stream length S2 is a multiple of K (K columns per step)
-  __device__ void fetch(int pos, int S2, In (&a)[D], int& kind) const {
+  // positions: [0, lead) sentinels, lead + j = column j (stream_lead above)
+  __device__ void fetch(int pos, int S2, int lead, In (&a)[D], int& kind) const {
 #pragma unroll
     for (int c = 0; c < D; c++) a[c] = (In)0;
     if (pos >= S2) {
       kind = 2;
-    } else if (pos == 0) {
+    } else if (pos < lead) {
       kind = 1;
     } else {
       kind = 0;
-      const int64_t col = min(pos - 1, m - 1);
+      const int64_t col = pos - lead;
 #pragma unroll
       for (int c = 0; c < D; c++) a[c] = __ldg(cols + col * D + c);
     }
@@ -359,10 +375,10 @@ struct LongRunner {
 
   // top value of position `pos` for this band: the corner/border for band 0,
   // else the producer's slot (spinning until its tag shows up)
-  __device__ __forceinline__ T top_of(int pos, int S2, bool has_in, const Link& in, unsigned tb,
+  __device__ __forceinline__ T top_of(int pos, int S2, int lead, bool has_in, const Link& in, unsigned tb,
                                       Pre pre) const {
     if (pos >= S2) return tinf<T>();
-    if (!has_in) return pos == 0 ? (T)0 : tinf<T>();
+    if (!has_in) return pos == lead - 1 ? (T)0 : tinf<T>();
     const unsigned want = tb + (unsigned)pos + 1u;
     if (!SL::ready(pre, want)) {
       const long long t0 = clock64();
@@ -415,7 +431,8 @@ struct LongRunner {
                            unsigned tbo, bool last_band, int out_idx, int* bad_flag) {
     static_assert(K == 2 || K == 4, "K columns per step");
     constexpr int P = 32 / K;                  // steps per 32-position chunk
-    const int S2 = (m + 1 + K - 1) / K * K;    // positions (a multiple of K)
+    const int lead = stream_lead<K>(m);
+    const int S2 = lead + m;                   // positions (a multiple of K)
     const int NT = S2 / K;                     // steps
     bool ok = true;
     T x[NS][R], c[R];
@@ -448,12 +465,12 @@ struct LongRunner {
     // a latency-bound warp); link slots of [32, 64) in flight
     In a[D], a2[D];
     int kind, kind2;
-    fetch(lane, S2, a, kind);
+    fetch(lane, S2, lead, a, kind);
     wait_chunk(31, S2, has_in, in, tbi);
     Pre pre = (has_in && lane < S2) ? SL::load(in.ring, in.mask, tbi + (unsigned)lane) : SL::none();
-    store_elem<K>(a, kind, lane, top_of(lane, S2, has_in, in, tbi, pre), ok);
-    fetch(32 + lane, S2, a, kind);
-    fetch(64 + lane, S2, a2, kind2);
+    store_elem<K>(a, kind, lane, top_of(lane, S2, lead, has_in, in, tbi, pre), ok);
+    fetch(32 + lane, S2, lead, a, kind);
+    fetch(64 + lane, S2, lead, a2, kind2);
     pre = (has_in && 32 + lane < S2) ? SL::load(in.ring, in.mask, tbi + (unsigned)(32 + lane)) : SL::none();
     __syncwarp();
     if (has_in && lane == 0) st_ctr(in.cons, tbi + (unsigned)min(32, S2));
@@ -463,6 +480,12 @@ struct LongRunner {
 
     const int total = NT + 31;
     const int pown = (has_out && lane == kWarp - 1) ? 1 : 0;
+    // DTW: the lane holding row n − 1 reads its value right after its last
+    // position (step NT − 1 + lane); later steps run it over the stream's end
+    // (d = +∞), which a sum does not survive
+    const int cap_lane = (n - 1 - r0) / R, cap_reg = (n - 1 - r0) - cap_lane * R;
+    const int t_cap = (FIN == F_DTW && last_band) ? NT + cap_lane : total + 1;
+    T dtw_val = tinf<T>();
     int t = 0, next_refill = P;
     while (t < total) {
       if (t == next_refill) {
@@ -475,11 +498,11 @@ struct LongRunner {
           const bool ready = pos >= S2 || SL::ready(pre, tbi + (unsigned)pos + 1u);
           if (!__all_sync(0xffffffffu, ready)) wait_chunk(p0 + 31, S2, has_in, in, tbi);
         }
-        store_elem<K>(a, kind, p0 + lane, top_of(p0 + lane, S2, has_in, in, tbi, pre), ok);
+        store_elem<K>(a, kind, p0 + lane, top_of(p0 + lane, S2, lead, has_in, in, tbi, pre), ok);
 #pragma unroll
         for (int cc = 0; cc < D; cc++) a[cc] = a2[cc];
         kind = kind2;
-        fetch(p0 + 64 + lane, S2, a2, kind2);
+        fetch(p0 + 64 + lane, S2, lead, a2, kind2);
         const int pn = p0 + 32 + lane;
         pre = (has_in && pn < S2) ? SL::load(in.ring, in.mask, tbi + (unsigned)pn) : SL::none();
         __syncwarp();
@@ -510,10 +533,10 @@ struct LongRunner {
         }
       }
       __syncwarp();
-      const int stop = min(next_refill, total);
+      const int stop = min(min(next_refill, total), t < t_cap ? t_cap : total);
       int g = t - lane;
       // primed again after every refill (its look-ahead may read unstored slots)
-      PipeK<T, KIND, D, R, INT_IN, K> pipe;
+      PipeK<T, KIND, D, R, INT_IN, K, FIN == F_DTW> pipe;
       pipe.prime(x, ring, g);
       // lane 31 publishes its K bottom-row values {value, tag} of every step with
       // predicated 16-byte stores (no divergent branch per step)
@@ -533,9 +556,20 @@ struct LongRunner {
         one(g);
         ++t;
       }
+      if constexpr (FIN == F_DTW) {
+        if (t == t_cap && lane == cap_lane) dtw_val = pick_reg<R>(c, cap_reg);
+      }
     }
     const bool all_ok = __all_sync(0xffffffffu, ok);
-    if (last_band && lane == kWarp - 1) {
+    if constexpr (FIN == F_DTW) {
+      // DTW: rows repeated below row n − 1 are not neutral for a sum, so the lane
+      // that holds row n − 1 emits, from its register (n − 1) mod R
+      if (last_band && lane == cap_lane) {
+        __threadfence();
+        const float f = (float)dtw_val;
+        reinterpret_cast<float*>(pb.out)[out_idx] = aborted(pb.abort) ? __int_as_float(0x7fc00000) : f;
+      }
+    } else if (last_band && lane == kWarp - 1) {
       __threadfence();
       const bool dead = aborted(pb.abort);
       if constexpr (INT_IN) {
@@ -668,7 +702,7 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
     int Rx;
     if (choose_r(n0 < m0 ? n0 : m0, Rx)) continue;
     const unsigned long long need_slots =
-        (unsigned long long)((min(n0, m0) + 2) & ~1) * Slots<T>::SPP;
+        (unsigned long long)stream_len<C::F ? kLCols : 2>(min(n0, m0)) * Slots<T>::SPP;
     unsigned long long cap = 2;
     while (cap < need_slots) cap <<= 1;
     if (cap <= pb.wrap_slots) wrap_mask = max(wrap_mask, (unsigned)(cap - 1ull));
@@ -729,7 +763,8 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
                      (swap ? pb.offsets[B + k] : pb.offsets[k]) * D;
     const In* cols = reinterpret_cast<const In*>(swap ? pb.p : pb.q) +
                      (swap ? pb.offsets[k] : pb.offsets[B + k]) * D;
-    const unsigned S = (unsigned)((m + 2) & ~1);  // stream positions of this pair (even, see run_band)
+    constexpr int KC = TIER64 ? 2 : kLCols;  // columns per step of this instantiation
+    const unsigned S = (unsigned)stream_len<KC>(m);  // stream positions of this pair (see run_band)
     if (multi && (unsigned long long)S * Slots<T>::SPP > (unsigned long long)wrap_mask + 1ull) {
       // the wrap ring cannot buffer this stream (both curves longer than the
       // band scratch holds: > 16M points, int64 tier 8M): documented limit, no plausible value
@@ -767,7 +802,7 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
           }
           const unsigned long long t0 = pb.trace ? gtimer() : 0ull;
           // fp32: four columns per step; int64 tier: two (its 64-bit state doubles the registers)
-          run.template run_band<TIER64 ? 2 : kLCols>(b * band_rows, has_in, lin, tb, has_out, lout, tbo,
+          run.template run_band<KC>(b * band_rows, has_in, lin, tb, has_out, lout, tbo,
                                                      b == nb - 1, k, pb.bad + li);
           if (pb.trace && lane == 0)
             printf("ffdtrace band %d cta %d warp %d start %llu end %llu\n", b, cta, warp, t0, gtimer());
@@ -906,10 +941,17 @@ cudaError_t launch_long_dim4(const LongArgs& a, int sms, cudaStream_t st, const 
 
 // fp32 input: one launch.  int32 input: the fp32-exact tier, then the exact
 // int64 tier over the pairs it flagged (a launch that exits at once when none is).
+// DTW (a.measure = 1, fp32 only): the + cell, sqrt per cell under L2.
 template <int D>
 cudaError_t launch_long_dim(const LongArgs& a, int sms, cudaStream_t st, const LongWs& w, int G,
                             int64_t* launches) {
   ++*launches;
+  if (a.measure == 1) {
+    if (a.norm == 1) return launch_long_k<float, K_L1, D, false, F_DTW>(a, sms, st, w, G);
+    if (a.norm == 3) return launch_long_k<float, K_LINF, D, false, F_DTW>(a, sms, st, w, G);
+    if (a.norm == 2) return launch_long_k<float, K_SQRT, D, false, F_DTW>(a, sms, st, w, G);
+    return launch_long_k<float, K_SQ, D, false, F_DTW>(a, sms, st, w, G);
+  }
   if (a.dtype != 1) {
     if (a.norm == 1) return launch_long_k<float, K_L1, D, false, F_NONE>(a, sms, st, w, G);
     if (a.norm == 3) return launch_long_k<float, K_LINF, D, false, F_NONE>(a, sms, st, w, G);

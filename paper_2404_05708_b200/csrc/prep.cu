@@ -27,10 +27,10 @@ __device__ __forceinline__ int pair_key(const int64_t* __restrict__ offsets,
   // fewer column steps, each with more rows to spread the step's fixed
   // shuffle/select/load cost over (always so when the longer curve fits one band).  δ_dF
   // is symmetric and its value is one of the d_ij, so either orientation gives
-  // the same bits; DTW (long_ok = 0) sums, so it keeps one orientation (the
+  // the same bits; DTW (long_ok < 0) sums, so it keeps one orientation (the
   // fp32 mirror's).
   bool tall = false;
-  if (long_ok) {
+  if (long_ok > 0) {
     // estimated issue cost nb · (cols + 32 window steps) · (9.5 + 3.5·R) of each
     // orientation (the step's fixed part + ~3.5 instructions per cell-row)
     const int lo = n < m ? n : m, hi = n < m ? m : n;
@@ -44,12 +44,12 @@ __device__ __forceinline__ int pair_key(const int64_t* __restrict__ offsets,
   const bool swap = tall ? n < m : n > m;
   const int rows = swap ? m : n, cols = swap ? n : m;
   const int nb = (rows + kWarp * kMaxR - 1) / (kWarp * kMaxR);
-  // DTW (long_ok = 0) has no long-pair path: only the pairs the batch kernel
-  // cannot hold leave it (with NaN); Fréchet also sends the medium ones
-  if (long_ok ? pair_goes_long(n, m, long_ok) : pair_too_long(n, m)) {
+  // DTW (long_ok < 0): only the pairs the batch kernel cannot hold go to the
+  // long-pair kernel; Fréchet (long_ok > 0) also sends the medium ones
+  if (long_ok == -2 || (long_ok > 0 ? pair_goes_long(n, m, long_ok) : pair_too_long(n, m))) {
     if (long_ok) {
       long_list[atomicAdd(long_count, 1)] = (int)k;
-    } else {  // no long-pair path for this measure (DTW): documented NaN
+    } else {  // no long-pair path requested: NaN
       if (int_out) reinterpret_cast<long long*>(out)[k] = LLONG_MIN;
       else reinterpret_cast<float*>(out)[k] = __int_as_float(0x7fc00000);
     }

@@ -64,8 +64,9 @@ struct BatchWs {
   size_t bytes;
 };
 
-// long_ok: 0 = no long-pair path (DTW: only pairs too long for the bands leave,
-// with NaN); else the medium-row threshold (medium_rows_for(B, SMs)) of Fréchet
+// long_ok: < 0 = DTW (only pairs too long for the bands go to the long-pair list),
+// 0 = no long-pair path (such pairs get NaN / INT64_MIN),
+// else the medium-row threshold (medium_rows_for(B, SMs)) of Fréchet
 cudaError_t launch_prep(const int64_t* offsets, const int32_t* lengths, int64_t B, int int_out,
                         int long_ok, void* out, const BatchWs& ws, int num_sms, cudaStream_t st,
                         int64_t* launches);

@@ -2,6 +2,8 @@
 against the CPU oracle: bit-exact against the fp32 mirror of the kernels'
 operation order, and within the rounding bound of an (n+m)-term fp32 sum of the
 fp64 oracle."""
+import os
+
 import numpy as np
 import pytest
 
@@ -80,13 +82,43 @@ def test_dtw_identity_and_unsupported(ffd):
         ffd.dtw_batch(pi, pi, o, ln, norm="sql2")
 
 
-def test_dtw_too_long_is_nan(ffd):
-    """no long-pair path for DTW: documented NaN (include/ffd.h)"""
+def _dtw_long_check(got, p, q, off, lens, norm, transposed):
+    B = len(lens) // 2
+    for k in range(B):
+        pk, qk = p[off[k]:off[k] + lens[k]], q[off[B + k]:off[B + k] + lens[B + k]]
+        ref = oracle.dtw_pair(pk, qk, norm)
+        tol = (lens[k] + lens[B + k] + 2 + 2) * 2.0 ** -24 * abs(ref)
+        assert abs(got[k] - ref) <= tol, (k, got[k], ref)
+        # bit-exact against the fp32 mirror in the kernel's orientation
+        mir = oracle.dtw_pair(qk, pk, norm, mirror=True) if transposed[k] else oracle.dtw_pair(pk, qk, norm, mirror=True)
+        assert got[k] == mir, (k, got[k], mir)
+
+
+@pytest.mark.parametrize("norm", ["l2", "l1"])
+def test_dtw_long_pairs(ffd, norm):
+    """Pairs too long for the batch kernel's bands (more than 16 bands of 512 rows)
+    run on the long-pair kernel with the DTW cell (round 1: documented NaN); the
+    kernel puts the shorter curve on the rows."""
     rng = np.random.default_rng(33)
-    p, q, off, lens = make(rng, [9000, 40, 9500, 50])   # 9000 rows: more than 16 bands
-    got = run(ffd, p, q, off, lens, "l2")
-    assert np.isnan(got[0])
-    assert got[1] == oracle.dtw_pair(p[off[1]:off[1] + 40], q[off[3]:off[3] + 50], "l2", mirror=True)
+    shapes = [(9000, 9500), (9600, 9000), (40, 50), (300, 9000)]
+    p, q, off, lens = make(rng, [a for a, _ in shapes] + [b for _, b in shapes])
+    got = run(ffd, p, q, off, lens, norm)
+    _dtw_long_check(got, p, q, off, lens, norm, [a > b for a, b in shapes])
+
+
+def test_dtw_long_multipass(ffd):
+    """A DTW pair on one or two CTAs: more bands than slots, several passes through
+    the wrap link (rows = the longer curve)."""
+    rng = np.random.default_rng(34)
+    shapes = [(8300, 9001), (9100, 8200)]
+    p, q, off, lens = make(rng, [a for a, _ in shapes] + [b for _, b in shapes])
+    for ctas in ("1", "2"):
+        os.environ["FFD_LONG_CTAS"] = ctas
+        try:
+            got = run(ffd, p, q, off, lens, "sql2")
+        finally:
+            del os.environ["FFD_LONG_CTAS"]
+        _dtw_long_check(got, p, q, off, lens, "sql2", [a < b for a, b in shapes])
 
 
 def test_dtw_medium_pairs_stay_on_batch_kernel(ffd):
@@ -98,3 +130,20 @@ def test_dtw_medium_pairs_stay_on_batch_kernel(ffd):
     got = run(ffd, p, q, off, lens, "sql2")
     assert np.isfinite(got).all()
     check(got, p, q, off, lens, 2, "sql2")
+
+
+@pytest.mark.parametrize("norm", ["sql2", "l1", "l2", "linf"])
+def test_dtw_long_kernel_small_shapes(ffd, norm):
+    """FFD_DTW_LONG=1 (testing) routes every DTW pair to the long-pair kernel: small
+    and odd shapes (1×1, one row, one column, odd/even column counts: one or two
+    leading sentinel positions) bit-exact against the fp32 mirror in the kernel's
+    orientation (the shorter curve on the rows)."""
+    rng = np.random.default_rng(35)
+    shapes = [(1, 1), (1, 2), (2, 1), (3, 4), (4, 3), (10, 12), (40, 50), (40, 51), (200, 333), (129, 64)]
+    p, q, off, lens = make(rng, [a for a, _ in shapes] + [b for _, b in shapes])
+    os.environ["FFD_DTW_LONG"] = "1"
+    try:
+        got = run(ffd, p, q, off, lens, norm)
+    finally:
+        del os.environ["FFD_DTW_LONG"]
+    _dtw_long_check(got, p, q, off, lens, norm, [a > b for a, b in shapes])

@@ -98,6 +98,18 @@ int ffd_batch_dtw(const void* p, const void* q, const int64_t* offsets, const in
                   int64_t num_pairs, int32_t dim, int32_t norm, int32_t dtype, void* out,
                   void* workspace, size_t workspace_bytes, ffd_stream_t stream);
 
+/* ffd_batch_dtw_f64 — DTW of B pairs with the sums (and every distance) in
+ *   fp64: the accumulation option of Appendix B's DTW.  Each
+ *   d_ij is evaluated in fp64 from the fp32 coordinates (Δ in fp64, squares
+ *   summed left to right, L2 one square root per cell) and every DP sum is one
+ *   fp64 rounding, so out[k] equals the fp64 oracle bit for bit.  dtype must be
+ *   FFD_F32; out: double[B]; same layout, workspace and stream semantics as
+ *   ffd_batch.  Limits: pairs too long for the batch kernel's bands (see
+ *   ffd_batch_dtw) get NaN — the long-pair kernel has no fp64 tier.           */
+int ffd_batch_dtw_f64(const void* p, const void* q, const int64_t* offsets, const int32_t* lengths,
+                      int64_t num_pairs, int32_t dim, int32_t norm, int32_t dtype, double* out,
+                      void* workspace, size_t workspace_bytes, ffd_stream_t stream);
+
 /* ffd_dist_sum — Σ_i Σ_j d(p_i, q_j) of each of B pairs: the paper's "upper
  *   limit" baseline, the distances of the DP workload
  *   (FFD_L2 takes a square root per cell, the paper's hypot L271) without the

@@ -56,6 +56,8 @@ def lib():
         L.ffd_batch.restype = ctypes.c_int
         L.ffd_batch_dtw.argtypes = [P, P, P, P, I64, I32_, I32_, I32_, P, P, SZ, P]
         L.ffd_batch_dtw.restype = ctypes.c_int
+        L.ffd_batch_dtw_f64.argtypes = [P, P, P, P, I64, I32_, I32_, I32_, P, P, SZ, P]
+        L.ffd_batch_dtw_f64.restype = ctypes.c_int
         L.ffd_dist_sum.argtypes = [P, P, P, P, I64, I32_, I32_, I32_, P, P]
         L.ffd_dist_sum.restype = ctypes.c_int
         L.ffd_batch_workspace_bytes.argtypes = [I64]
@@ -86,7 +88,7 @@ def lib():
     return _lib
 
 
-EXPORTED = ["ffd_batch", "ffd_batch_dtw", "ffd_dist_sum", "ffd_batch_workspace_bytes", "ffd_batch_host", "ffd_cdist",
+EXPORTED = ["ffd_batch", "ffd_batch_dtw", "ffd_batch_dtw_f64", "ffd_dist_sum", "ffd_batch_workspace_bytes", "ffd_batch_host", "ffd_cdist",
             "ffd_cdist_workspace_bytes", "ffd_cdist_self", "ffd_cdist_to", "ffd_validate_batch", "ffd_status_string",
             "ffd_take_launch_count", "ffd_version", "ffd_profile_enable", "ffd_profile_take"]
 
@@ -176,7 +178,8 @@ def batch(p, q, offsets, lengths, norm="l2", out=None, stream=None, measure="fre
     """δ_dF for B pairs (ffd_batch).  p [Σn, dim], q [Σm, dim] float32/int32 CUDA
     tensors; offsets int64[2B]; lengths int32[2B].  Returns float32[B] (fp32
     input) or int64[B] (int32 input).  measure="dtw": dynamic time warping
-    (ffd_batch_dtw, PAPER Appendix B; float32 input only).  validate=True first
+    (ffd_batch_dtw, PAPER Appendix B; float32 input only); measure="dtw_f64": the
+    same with fp64 sums (ffd_batch_dtw_f64, float64[B]).  validate=True first
     runs ffd_validate_batch (synchronous) and raises FFDError on empty curves,
     offsets out of range, non-finite coordinates or int64 overflow; with
     validate=False such pairs give NaN / INT64_MIN (or are undefined).  Inside a
@@ -185,26 +188,31 @@ def batch(p, q, offsets, lengths, norm="l2", out=None, stream=None, measure="fre
     dt, p, q, offsets, lengths = _batch_args(p, q, offsets, lengths)
     B = offsets.numel() // 2
     dim = p.shape[1]
-    if measure not in ("frechet", "dtw"):
+    fns = {"frechet": "ffd_batch", "dtw": "ffd_batch_dtw", "dtw_f64": "ffd_batch_dtw_f64"}
+    if measure not in fns:
         raise ValueError(f"unknown measure {measure!r}")
     if validate and not torch.cuda.is_current_stream_capturing():  # (a synchronous check cannot be captured)
         _check(int(lib().ffd_validate_batch(p.data_ptr(), p.shape[0], q.data_ptr(), q.shape[0],
                                             offsets.data_ptr(), lengths.data_ptr(), B, dim, dt,
                                             _stream_ptr(stream))), "ffd_validate_batch")
     if out is None:
-        out = torch.empty(B, dtype=torch.int64 if dt == I32 else torch.float32, device=p.device)
+        odt = torch.float64 if measure == "dtw_f64" else (torch.int64 if dt == I32 else torch.float32)
+        out = torch.empty(B, dtype=odt, device=p.device)
     ws_bytes = lib().ffd_batch_workspace_bytes(B)
     ws = workspace(ws_bytes, p.device, stream)
-    fn = lib().ffd_batch if measure == "frechet" else lib().ffd_batch_dtw
+    fn = getattr(lib(), fns[measure])
     _check(fn(p.data_ptr(), q.data_ptr(), offsets.data_ptr(), lengths.data_ptr(), B, dim,
-              _norm(norm), dt, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)),
-           "ffd_batch" if measure == "frechet" else "ffd_batch_dtw")
+              _norm(norm), dt, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)), fns[measure])
     return out
 
 
-def dtw_batch(p, q, offsets, lengths, norm="l2", out=None, stream=None, validate=True):
-    """Dynamic time warping of B pairs (ffd_batch_dtw): same layout as batch()."""
-    return batch(p, q, offsets, lengths, norm=norm, out=out, stream=stream, measure="dtw", validate=validate)
+def dtw_batch(p, q, offsets, lengths, norm="l2", out=None, stream=None, validate=True, precision="f32"):
+    """Dynamic time warping of B pairs (ffd_batch_dtw, or ffd_batch_dtw_f64 with
+    precision="f64": fp64 sums, bit-exact against the fp64 oracle): same layout as batch()."""
+    if precision not in ("f32", "f64"):
+        raise ValueError("precision must be 'f32' or 'f64'")
+    return batch(p, q, offsets, lengths, norm=norm, out=out, stream=stream,
+                 measure="dtw" if precision == "f32" else "dtw_f64", validate=validate)
 
 
 def dist_sum(p, q, offsets, lengths, norm="l2", out=None, stream=None):

@@ -130,14 +130,14 @@ static int check_common(int32_t dim, int32_t norm, int32_t dtype) {
   return FFD_OK;
 }
 
-// measure: 0 discrete Fréchet (Eq. (1)), 1 DTW (Appendix B)
+// measure: 0 discrete Fréchet (Eq. (1)), 1 DTW (Appendix B), 2 DTW in fp64
 static int batch_impl(const void* p, const void* q, const int64_t* offsets, const int32_t* lengths,
                       int64_t B, int32_t dim, int32_t norm, int32_t dtype, void* out,
                       void* workspace, size_t ws_bytes, cudaStream_t st, int measure = 0,
                       bool long_possible = true) {
   int s = check_common(dim, norm, dtype);
   if (s) return s;
-  if (measure == 1 && dtype != FFD_F32) return FFD_ERR_UNSUPPORTED;
+  if (measure != 0 && dtype != FFD_F32) return FFD_ERR_UNSUPPORTED;
   if (B < 0) return FFD_ERR_ARG;
   if (B == 0) return FFD_OK;
   if (!p || !q || !offsets || !lengths || !out) return FFD_ERR_ARG;
@@ -149,11 +149,11 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
   const int int_in = dtype == FFD_I32;
   int kind = kind_for(norm, dtype);
   int fin = (norm == FFD_L2) ? F_SQRT : F_NONE;
-  if (measure == 1) {  // DTW: L2 needs the per-cell square root (sums do not commute with it)
+  if (measure != 0) {  // DTW: L2 needs the per-cell square root (sums do not commute with it)
     if (norm == FFD_L2) kind = K_SQRT;
     fin = F_DTW;
   }
-  const BatchEntry* main_e = find_batch(BatchKey{0, kind, dim, int_in, fin});
+  const BatchEntry* main_e = find_batch(BatchKey{measure == 2 ? 2 : 0, kind, dim, int_in, fin});
   if (!main_e) return FFD_ERR_UNSUPPORTED;
   const BatchEntry* fb_e = nullptr;
   if (int_in) {
@@ -165,8 +165,10 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
   // Fréchet: pairs too long for the bands, and the medium ones, go to the long-pair
   // kernel; DTW (−1): only those too long for the bands (its sums keep one orientation)
   const bool dtw_all_long = measure == 1 && getenv("FFD_DTW_LONG") != nullptr;  // testing: every DTW pair long
-  const int long_ok = measure == 0 ? medium_rows_for(B, di.sms) : (dtw_all_long ? -2 : -1);
-  if (launch_prep(offsets, lengths, B, int_in, long_ok, out, ws, di.sms, st, &g_launches) !=
+  // (the fp64 DTW tier has no long-pair path: 0, such pairs get NaN)
+  const int long_ok = measure == 0 ? medium_rows_for(B, di.sms) : measure == 2 ? 0 : (dtw_all_long ? -2 : -1);
+  const int out_kind = int_in ? 1 : (measure == 2 ? 2 : 0);
+  if (launch_prep(offsets, lengths, B, out_kind, long_ok, out, ws, di.sms, st, &g_launches) !=
       cudaSuccess)
     return FFD_ERR_CUDA;
 
@@ -187,6 +189,8 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
   int occ = main_e->occupancy();
   if (occ < 1) occ = 1;
   if (occ > kMaxCtasMain) occ = kMaxCtasMain;
+  // fp64 DTW: 8-byte band scratch in the float-sized buffer holds half the warps
+  if (measure == 2 && occ > kMaxCtasMain / 2) occ = kMaxCtasMain / 2;
   {
     // chunk size: kChunkPairs, unless the batch is too small to give every
     // resident warp at least one chunk (then fewer pairs per chunk)
@@ -220,7 +224,7 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
     ++g_launches;
   }
 
-  if (!long_possible) return FFD_OK;  // the caller saw every length: no pair is long
+  if (!long_possible || measure == 2) return FFD_OK;  // no pair is long (caller saw every length), or fp64 DTW
   // pairs too long for the band scratch of the batch kernel: cross-CTA wavefront
   LongArgs la{};
   la.p = p;
@@ -399,6 +403,13 @@ int ffd_batch_dtw(const void* p, const void* q, const int64_t* offsets, const in
                   void* workspace, size_t workspace_bytes, ffd_stream_t stream) {
   return batch_impl(p, q, offsets, lengths, num_pairs, dim, norm, dtype, out, workspace,
                     workspace_bytes, reinterpret_cast<cudaStream_t>(stream), 1);
+}
+
+int ffd_batch_dtw_f64(const void* p, const void* q, const int64_t* offsets, const int32_t* lengths,
+                      int64_t num_pairs, int32_t dim, int32_t norm, int32_t dtype, double* out,
+                      void* workspace, size_t workspace_bytes, ffd_stream_t stream) {
+  return batch_impl(p, q, offsets, lengths, num_pairs, dim, norm, dtype, out, workspace,
+                    workspace_bytes, reinterpret_cast<cudaStream_t>(stream), 2);
 }
 
 int ffd_dist_sum(const void* p, const void* q, const int64_t* offsets, const int32_t* lengths,

@@ -10,6 +10,14 @@
 
 namespace ffd {
 
+// the invalid-output value of pair k: INT64_MIN (int64 out), NaN (float or double out)
+// out_kind (the `int_out` argument): 0 float, 1 int64, 2 double
+__device__ __forceinline__ void write_invalid(void* out, int64_t k, int out_kind) {
+  if (out_kind == 1) reinterpret_cast<long long*>(out)[k] = LLONG_MIN;
+  else if (out_kind == 2) reinterpret_cast<double*>(out)[k] = __longlong_as_double(0x7ff8000000000000ll);
+  else reinterpret_cast<float*>(out)[k] = __int_as_float(0x7fc00000);
+}
+
 // shape key of pair k, and its descriptor; −1 when the pair is dropped (its
 // invalid-output value written, or sent to the long-pair list)
 __device__ __forceinline__ int pair_key(const int64_t* __restrict__ offsets,
@@ -18,8 +26,7 @@ __device__ __forceinline__ int pair_key(const int64_t* __restrict__ offsets,
                                         int* __restrict__ long_list, int* __restrict__ long_count) {
   const int n = lengths[k], m = lengths[B + k];
   if (n < 1 || m < 1) {
-    if (int_out) reinterpret_cast<long long*>(out)[k] = LLONG_MIN;
-    else reinterpret_cast<float*>(out)[k] = __int_as_float(0x7fc00000);
+    write_invalid(out, k, int_out);
     return -1;
   }
   // Orientation: the rows (held in registers, R per lane) are the shorter curve,
@@ -50,8 +57,7 @@ __device__ __forceinline__ int pair_key(const int64_t* __restrict__ offsets,
     if (long_ok) {
       long_list[atomicAdd(long_count, 1)] = (int)k;
     } else {  // no long-pair path requested: NaN
-      if (int_out) reinterpret_cast<long long*>(out)[k] = LLONG_MIN;
-      else reinterpret_cast<float*>(out)[k] = __int_as_float(0x7fc00000);
+      write_invalid(out, k, int_out);
     }
     return -1;
   }

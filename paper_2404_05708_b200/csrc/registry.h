@@ -10,7 +10,7 @@ namespace ffd {
 struct Problem;
 
 struct BatchKey {
-  int tier;    // 0: fp32 main tier, 1: exact int64 fallback tier
+  int tier;    // 0: fp32 main tier, 1: exact int64 fallback tier, 2: fp64 DTW tier
   int kind;    // Kind
   int dim;
   int int_in;  // input coordinates int32

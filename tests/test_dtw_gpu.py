@@ -147,3 +147,35 @@ def test_dtw_long_kernel_small_shapes(ffd, norm):
     finally:
         del os.environ["FFD_DTW_LONG"]
     _dtw_long_check(got, p, q, off, lens, norm, [a > b for a, b in shapes])
+
+
+def run64(ffd, p, q, off, lens, norm, validate=True):
+    args = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (p, q, off, lens)]
+    return ffd.dtw_batch(*args, norm=norm, precision="f64", validate=validate).cpu().numpy()
+
+
+@pytest.mark.parametrize("dim", [1, 2, 3, 4])
+@pytest.mark.parametrize("norm", ["l2", "sql2", "l1", "linf"])
+def test_dtw_f64_bit_exact(ffd, norm, dim):
+    """ffd_batch_dtw_f64: fp64 distances in the oracle's operation order and fp64
+    sums, so every result equals the fp64 oracle (orc_pair_dtw_f32) bit for bit —
+    the tight tolerance the fp32 path cannot have ((n+m+D+2)·2⁻²⁴)."""
+    rng = np.random.default_rng(700 + dim * 11 + len(norm))
+    lens = rng.integers(1, 700, size=2 * 80)
+    lens[:4] = [1, 257, 300, 1024]       # one point; more than one 256-row band (fp64 bands: R ≤ 8)
+    lens[80:84] = [5, 1, 900, 333]
+    p, q, off, lens = make(rng, lens, dim=dim)
+    got = run64(ffd, p, q, off, lens, norm)
+    ref = oracle.dtw_batch(p, q, off, lens, dim, norm)
+    assert got.dtype == np.float64
+    bad = np.flatnonzero(got != ref)
+    assert bad.size == 0, (bad[:5], got[bad[:5]], ref[bad[:5]])
+
+
+def test_dtw_f64_edges(ffd):
+    rng = np.random.default_rng(36)
+    p, q, off, lens = make(rng, [5, 0, 9000, 7, 6, 40, 9500, 0])
+    got = run64(ffd, p, q, off, lens, "l2", validate=False)
+    assert np.isnan(got[1]) and np.isnan(got[3])   # empty curves
+    assert np.isnan(got[2])                        # too long for the bands: no fp64 long-pair tier
+    assert got[0] == oracle.dtw_pair(p[off[0]:off[0] + 5], q[off[4]:off[4] + 6], "l2")

@@ -194,6 +194,32 @@ int ffd_cdist_to(const void* setA, int64_t nA, int32_t lenA, const void* setB, i
                  size_t workspace_bytes, ffd_stream_t stream);
 
 /* ---------------------------------------------------------------------------
+ * ffd_long_pair_shard — one very long pair over several GPUs.
+ *   The rows curve (the shorter of p, q; p on a tie) is split into row ranges,
+ *   one per GPU; each GPU runs this call on its range [row_begin, row_end) and
+ *   the band chain of Eq. (1) (linear memory: Theorem 1)
+ *   continues across GPUs: the first band of a range reads its top input from
+ *   in_ring (in THIS GPU's memory, written by the GPU of the range above over
+ *   NVLink) and the last band writes its bottom row into out_ring (the NEXT
+ *   GPU's in_ring, a peer pointer mapped into this context: CUDA IPC or torch
+ *   symmetric memory).  Rings hold a whole stream of ffd_long_pair_ring_bytes()
+ *   bytes, so a GPU never waits for its consumer: the calls may run
+ *   concurrently (pipelined over NVLink) or one after another (the same
+ *   result).  The GPU whose range ends at the last row writes out[0] = δ_dF.
+ *   p: [n, dim], q: [m, dim] fp32 (FFD_F32 only), device pointers, identical on
+ *   every GPU.  row_begin is a multiple of ffd_long_pair_row_align() (512) and
+ *   so is row_end unless it is the last row.  Tag bases: both ends of a link
+ *   pass the same in/out tag base per call and advance it by at least the
+ *   ring's slot count (bytes / 8) from one call to the next; a ring must be
+ *   zeroed before its first use.  Returns FFD_ERR_ARG for bad ranges or rings.  */
+size_t ffd_long_pair_ring_bytes(int32_t n, int32_t m);
+int32_t ffd_long_pair_row_align(void);
+int ffd_long_pair_shard(const void* p, int32_t n, const void* q, int32_t m, int32_t dim, int32_t norm,
+                        int32_t dtype, int32_t row_begin, int32_t row_end, void* in_ring, size_t in_ring_bytes,
+                        uint32_t in_tag_base, void* out_ring, size_t out_ring_bytes, uint32_t out_tag_base,
+                        void* out, ffd_stream_t stream);
+
+/* ---------------------------------------------------------------------------
  * ffd_validate_batch — SYNCHRONOUS device-data precondition check of a batch:
  *   lengths ≥ 1 (FFD_ERR_EMPTY), offsets+lengths within [0, np)/[0, nq)
  *   (FFD_ERR_RANGE), finite fp32 coordinates (FFD_ERR_NONFINITE), and for int32

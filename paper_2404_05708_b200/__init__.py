@@ -73,6 +73,13 @@ def lib():
         L.ffd_cdist_to.restype = ctypes.c_int
         L.ffd_cdist_workspace_bytes.argtypes = []
         L.ffd_cdist_workspace_bytes.restype = SZ
+        L.ffd_long_pair_ring_bytes.argtypes = [I32_, I32_]
+        L.ffd_long_pair_ring_bytes.restype = SZ
+        L.ffd_long_pair_row_align.argtypes = []
+        L.ffd_long_pair_row_align.restype = I32_
+        L.ffd_long_pair_shard.argtypes = [P, I32_, P, I32_, I32_, I32_, I32_, I32_, I32_, P, SZ, ctypes.c_uint32,
+                                          P, SZ, ctypes.c_uint32, P, P]
+        L.ffd_long_pair_shard.restype = ctypes.c_int
         L.ffd_validate_batch.argtypes = [P, I64, P, I64, P, P, I64, I32_, I32_, P]
         L.ffd_validate_batch.restype = ctypes.c_int
         L.ffd_status_string.argtypes = [ctypes.c_int]
@@ -89,7 +96,8 @@ def lib():
 
 
 EXPORTED = ["ffd_batch", "ffd_batch_dtw", "ffd_batch_dtw_f64", "ffd_dist_sum", "ffd_batch_workspace_bytes", "ffd_batch_host", "ffd_cdist",
-            "ffd_cdist_workspace_bytes", "ffd_cdist_self", "ffd_cdist_to", "ffd_validate_batch", "ffd_status_string",
+            "ffd_cdist_workspace_bytes", "ffd_cdist_self", "ffd_cdist_to", "ffd_long_pair_ring_bytes",
+            "ffd_long_pair_row_align", "ffd_long_pair_shard", "ffd_validate_batch", "ffd_status_string",
             "ffd_take_launch_count", "ffd_version", "ffd_profile_enable", "ffd_profile_take"]
 
 
@@ -312,6 +320,37 @@ def cdist_to(A, B, outs, ld_out, norm="l2", rows=None, self_mode=False, col_offs
                               1 if self_mode else 0, col_offset, 1 if mirror else 0, ptrs, len(outs), ld_out,
                               ws.data_ptr() if ws is not None else None, wsb, _stream_ptr(stream)),
            "ffd_cdist_to")
+
+
+def long_pair_ring_bytes(n: int, m: int) -> int:
+    """Bytes of one cross-GPU ring of ffd_long_pair_shard for an n×m pair."""
+    return int(lib().ffd_long_pair_ring_bytes(n, m))
+
+
+def long_pair_row_align() -> int:
+    return int(lib().ffd_long_pair_row_align())
+
+
+def long_pair_shard(p, q, rows, norm="l2", in_ring=None, in_tag=0, out_ring=None, out_tag=0, out=None,
+                    stream=None):
+    """ffd_long_pair_shard: rows = (row_begin, row_end) of the rows curve (the shorter
+    of p, q) on this GPU; in_ring: a local uint8 CUDA tensor (or None for the first
+    range); out_ring: (pointer, bytes) of the next GPU's ring (or None for the last
+    range).  Returns `out` (float32[1]); only the range ending at the last row
+    writes δ into it."""
+    torch = _torch()
+    if _dtype_code(p) != F32 or q.dtype != p.dtype:
+        raise FFDError(-2, "ffd_long_pair_shard")
+    p, q = p.contiguous(), q.contiguous()
+    if out is None:
+        out = torch.full((1,), float("nan"), dtype=torch.float32, device=p.device)
+    in_ptr, in_b = (in_ring.data_ptr(), in_ring.numel()) if in_ring is not None else (None, 0)
+    out_ptr, out_b = (int(out_ring[0]), int(out_ring[1])) if out_ring is not None else (None, 0)
+    _check(lib().ffd_long_pair_shard(p.data_ptr(), p.shape[0], q.data_ptr(), q.shape[0], p.shape[1], _norm(norm),
+                                     F32, rows[0], rows[1], in_ptr, in_b, in_tag & 0xffffffff, out_ptr, out_b,
+                                     out_tag & 0xffffffff, out.data_ptr(), _stream_ptr(stream)),
+           "ffd_long_pair_shard")
+    return out
 
 
 def validate(p, q, offsets, lengths, stream=None) -> int:

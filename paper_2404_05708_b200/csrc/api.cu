@@ -645,6 +645,50 @@ int ffd_cdist_to(const void* setA, int64_t nA, int32_t lenA, const void* setB, i
                       workspace, workspace_bytes, stream);
 }
 
+size_t ffd_long_pair_ring_bytes(int32_t n, int32_t m) {
+  if (n < 1 || m < 1) return 0;
+  return long_shard_ring_slots(n > m ? n : m) * 8;
+}
+
+int32_t ffd_long_pair_row_align(void) { return kWarp * kMaxR; }
+
+int ffd_long_pair_shard(const void* p, int32_t n, const void* q, int32_t m, int32_t dim, int32_t norm,
+                        int32_t dtype, int32_t row_begin, int32_t row_end, void* in_ring, size_t in_ring_bytes,
+                        uint32_t in_tag_base, void* out_ring, size_t out_ring_bytes, uint32_t out_tag_base,
+                        void* out, ffd_stream_t stream) {
+  int s = check_common(dim, norm, dtype);
+  if (s) return s;
+  if (dtype != FFD_F32) return FFD_ERR_UNSUPPORTED;
+  if (!p || !q || !out || n < 1 || m < 1) return FFD_ERR_ARG;
+  const int rows = n < m ? n : m;  // the shorter curve is the rows curve (p on a tie)
+  const int align = ffd_long_pair_row_align();
+  if (row_begin < 0 || row_end <= row_begin || row_end > rows) return FFD_ERR_ARG;
+  if (row_begin % align || (row_end != rows && row_end % align)) return FFD_ERR_ARG;
+  const size_t need = ffd_long_pair_ring_bytes(n, m);
+  if (row_begin > 0 && (!in_ring || in_ring_bytes < need)) return FFD_ERR_ARG;
+  if (row_end < rows && (!out_ring || out_ring_bytes < need)) return FFD_ERR_ARG;
+  LongArgs la{};
+  la.p = p;
+  la.q = q;
+  la.dim = dim;
+  la.norm = norm;
+  la.dtype = dtype;
+  la.out = out;
+  la.row_begin = row_begin;
+  la.row_end = row_end;
+  la.ext_in = row_begin > 0 ? in_ring : nullptr;
+  la.ext_in_slots = row_begin > 0 ? need / 8 : 0;
+  la.ext_in_tb = in_tag_base;
+  la.ext_out = row_end < rows ? out_ring : nullptr;
+  la.ext_out_slots = row_end < rows ? need / 8 : 0;
+  la.ext_out_tb = out_tag_base;
+  ProfScope prof(reinterpret_cast<cudaStream_t>(stream), 2);
+  return launch_long_shard(la, n, m, dev_info().sms, reinterpret_cast<cudaStream_t>(stream), &g_launches) ==
+                 cudaSuccess
+             ? FFD_OK
+             : FFD_ERR_CUDA;
+}
+
 int ffd_validate_batch(const void* p, int64_t np, const void* q, int64_t nq,
                        const int64_t* offsets, const int32_t* lengths, int64_t num_pairs,
                        int32_t dim, int32_t dtype, ffd_stream_t stream) {

@@ -17,6 +17,21 @@ struct LongArgs {
   void* out;
   void* wrap;         // device scratch for the multi-pass wrap link (any contents)
   size_t wrap_bytes;  // its size
+  // ffd_long_pair_shard: rows [row_begin, row_end) of the single pair, links to the
+  // neighbouring GPUs' rings (slots are 8-byte {value, tag}; sizes powers of two)
+  int shard;
+  int row_begin, row_end;
+  void* ext_in;
+  size_t ext_in_slots;
+  unsigned ext_in_tb;
+  void* ext_out;
+  size_t ext_out_slots;
+  unsigned ext_out_tb;
+  unsigned* ext_cons;  // [2] device
 };
 cudaError_t launch_long_pairs(const LongArgs& a, int sms, cudaStream_t st, int64_t* launches);
+// slots of a cross-GPU ring for a pair whose column curve has m points (fp32)
+size_t long_shard_ring_slots(int m);
+// one pair (n rows after orientation = the shorter curve), rows [row_begin, row_end)
+cudaError_t launch_long_shard(LongArgs a, int n0, int m0, int sms, cudaStream_t st, int64_t* launches);
 }  // namespace ffd

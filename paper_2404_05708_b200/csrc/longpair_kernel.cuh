@@ -99,6 +99,18 @@ struct LongProblem {
   int* abort;      // a watchdog fired: every spin gives up, results become NaN / INT64_MIN
   int trace;       // FFD_LONG_TRACE=1: print each band's start/end time
   int force_r;     // FFD_LONG_R (testing): rows per lane instead of the automatic choice
+  // ffd_long_pair_shard (one pair, its rows curve split over GPUs): this launch
+  // computes rows [row_begin, row_end); its first band reads its top input from
+  // ext_in (a ring in this GPU's memory that the previous GPU writes over NVLink)
+  // and its last band writes its bottom row into ext_out (the next GPU's ring).
+  // The rings hold a whole stream, so no flow control crosses GPUs.
+  int shard;
+  int row_begin, row_end;
+  uint2* ext_in;
+  unsigned ext_in_mask, ext_in_tb;
+  uint2* ext_out;
+  unsigned ext_out_mask, ext_out_tb;
+  unsigned* ext_cons;  // [2]: the consumer's progress (unread), the producer's (stays at ext_out_tb)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -107,26 +119,43 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-__device__ __forceinline__ uint2 ld_slot(const uint2* p) {
+// slot accesses; `sys` selects system scope for links whose ring is written by
+// another GPU over NVLink (the cross-GPU links of ffd_long_pair_shard)
+__device__ __forceinline__ uint2 ld_slot(const uint2* p, int sys = 0) {
   uint2 v;
-  asm volatile("ld.relaxed.gpu.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
+  if (sys)
+    asm volatile("ld.relaxed.sys.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
+  else
+    asm volatile("ld.relaxed.gpu.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ uint4 ld_slot4(const uint2* p) {
+__device__ __forceinline__ uint4 ld_slot4(const uint2* p, int sys = 0) {
   uint4 v;
-  asm volatile("ld.relaxed.gpu.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p)
-               : "memory");
+  if (sys)
+    asm volatile("ld.relaxed.sys.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p)
+                 : "memory");
+  else
+    asm volatile("ld.relaxed.gpu.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p)
+                 : "memory");
   return v;
 }
 // one predicated 16-byte store {a, b, c, d} (no divergent branch per step)
 __device__ __forceinline__ void st_v4_pred(uint2* p, unsigned a, unsigned b, unsigned c, unsigned d,
-                                           int pred) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %5, 0;\n\t@q st.relaxed.gpu.v4.u32 [%0], {%1, %2, %3, %4};\n\t}" ::"l"(p),
-      "r"(a), "r"(b), "r"(c), "r"(d), "r"(pred)
-      : "memory");
+                                           int pred, int sys = 0) {
+  if (sys)
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %5, 0;\n\t@q st.relaxed.sys.v4.u32 [%0], {%1, %2, %3, %4};\n\t}" ::"l"(p),
+        "r"(a), "r"(b), "r"(c), "r"(d), "r"(pred)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %5, 0;\n\t@q st.relaxed.gpu.v4.u32 [%0], {%1, %2, %3, %4};\n\t}" ::"l"(p),
+        "r"(a), "r"(b), "r"(c), "r"(d), "r"(pred)
+        : "memory");
 }
 __device__ __forceinline__ unsigned ld_ctr(const unsigned* p) {
   unsigned v;
@@ -148,24 +177,24 @@ template <>
 struct Slots<float> {  // one slot per position
   static constexpr unsigned SPP = 1;
   using Pre = uint2;
-  static __device__ __forceinline__ Pre load(const uint2* ring, unsigned mask, unsigned A) {
-    return ld_slot(ring + (A & mask));
+  static __device__ __forceinline__ Pre load(const uint2* ring, unsigned mask, unsigned A, int sys = 0) {
+    return ld_slot(ring + (A & mask), sys);
   }
   static __device__ __forceinline__ bool ready(const Pre& v, unsigned want) { return v.y == want; }
   static __device__ __forceinline__ float value(const Pre& v) { return __uint_as_float(v.x); }
   static __device__ __forceinline__ Pre none() { return make_uint2(0u, 0u); }
   // positions A (even) and A+1 in one 16-byte store
   static __device__ __forceinline__ void put2(uint2* ring, unsigned mask, unsigned A, float v0, float v1,
-                                              int pred) {
-    st_v4_pred(ring + (A & mask & ~1u), __float_as_uint(v0), A + 1u, __float_as_uint(v1), A + 2u, pred);
+                                              int pred, int sys = 0) {
+    st_v4_pred(ring + (A & mask & ~1u), __float_as_uint(v0), A + 1u, __float_as_uint(v1), A + 2u, pred, sys);
   }
 };
 template <>
 struct Slots<long long> {  // two slots per position: {lo, tag}, {hi, tag}
   static constexpr unsigned SPP = 2;
   using Pre = uint4;
-  static __device__ __forceinline__ Pre load(const uint2* ring, unsigned mask, unsigned A) {
-    return ld_slot4(ring + ((2u * A) & mask));
+  static __device__ __forceinline__ Pre load(const uint2* ring, unsigned mask, unsigned A, int sys = 0) {
+    return ld_slot4(ring + ((2u * A) & mask), sys);
   }
   static __device__ __forceinline__ bool ready(const Pre& v, unsigned want) {
     return v.y == want && v.w == want;
@@ -175,11 +204,11 @@ struct Slots<long long> {  // two slots per position: {lo, tag}, {hi, tag}
   }
   static __device__ __forceinline__ Pre none() { return make_uint4(0u, 0u, 0u, 0u); }
   static __device__ __forceinline__ void put2(uint2* ring, unsigned mask, unsigned A, long long v0,
-                                              long long v1, int pred) {
+                                              long long v1, int pred, int sys = 0) {
     uint2* s = ring + ((2u * A) & mask);  // 32-byte aligned: A is even
     const unsigned long long u0 = (unsigned long long)v0, u1 = (unsigned long long)v1;
-    st_v4_pred(s, (unsigned)u0, A + 1u, (unsigned)(u0 >> 32), A + 1u, pred);
-    st_v4_pred(s + 2, (unsigned)u1, A + 2u, (unsigned)(u1 >> 32), A + 2u, pred);
+    st_v4_pred(s, (unsigned)u0, A + 1u, (unsigned)(u0 >> 32), A + 1u, pred, sys);
+    st_v4_pred(s + 2, (unsigned)u1, A + 2u, (unsigned)(u1 >> 32), A + 2u, pred, sys);
   }
 };
 
@@ -188,6 +217,7 @@ struct Link {
   uint2* ring;
   unsigned mask;
   unsigned* cons;
+  int sys;  // written by another GPU (system-scope accesses)
 };
 
 constexpr int kLRing = 256;  // column-ring positions per warp: lane 31 trails lane 0 by 31·K ≤ 124
@@ -383,7 +413,7 @@ struct LongRunner {
     if (!SL::ready(pre, want)) {
       const long long t0 = clock64();
       while (!SL::ready(pre, want)) {
-        pre = SL::load(in.ring, in.mask, tb + (unsigned)pos);
+        pre = SL::load(in.ring, in.mask, tb + (unsigned)pos, in.sys);
         // the abort flag is an L2 round trip: read it only in a long wait
         if (clock64() - t0 > kAbortCheckCycles && aborted(pb.abort)) break;
         if (clock64() - t0 > kWatchdogCycles) {  // a link that never delivers: report, abort
@@ -407,9 +437,9 @@ struct LongRunner {
     if (has_in && lane == 0) {
       pos = min(pos, S2 - 1);
       const unsigned want = tb + (unsigned)pos + 1u;
-      if (!SL::ready(SL::load(in.ring, in.mask, tb + (unsigned)pos), want)) {
+      if (!SL::ready(SL::load(in.ring, in.mask, tb + (unsigned)pos, in.sys), want)) {
         const long long t0 = clock64();
-        while (!SL::ready(SL::load(in.ring, in.mask, tb + (unsigned)pos), want)) {
+        while (!SL::ready(SL::load(in.ring, in.mask, tb + (unsigned)pos, in.sys), want)) {
           __nanosleep(64);
           if (clock64() - t0 > kAbortCheckCycles && aborted(pb.abort)) break;
           if (clock64() - t0 > kWatchdogCycles) {
@@ -467,11 +497,11 @@ struct LongRunner {
     int kind, kind2;
     fetch(lane, S2, lead, a, kind);
     wait_chunk(31, S2, has_in, in, tbi);
-    Pre pre = (has_in && lane < S2) ? SL::load(in.ring, in.mask, tbi + (unsigned)lane) : SL::none();
+    Pre pre = (has_in && lane < S2) ? SL::load(in.ring, in.mask, tbi + (unsigned)lane, in.sys) : SL::none();
     store_elem<K>(a, kind, lane, top_of(lane, S2, lead, has_in, in, tbi, pre), ok);
     fetch(32 + lane, S2, lead, a, kind);
     fetch(64 + lane, S2, lead, a2, kind2);
-    pre = (has_in && 32 + lane < S2) ? SL::load(in.ring, in.mask, tbi + (unsigned)(32 + lane)) : SL::none();
+    pre = (has_in && 32 + lane < S2) ? SL::load(in.ring, in.mask, tbi + (unsigned)(32 + lane), in.sys) : SL::none();
     __syncwarp();
     if (has_in && lane == 0) st_ctr(in.cons, tbi + (unsigned)min(32, S2));
     const unsigned cap = (out.mask + 1u) / SL::SPP;  // output ring capacity in positions
@@ -504,7 +534,7 @@ struct LongRunner {
         kind = kind2;
         fetch(p0 + 64 + lane, S2, lead, a2, kind2);
         const int pn = p0 + 32 + lane;
-        pre = (has_in && pn < S2) ? SL::load(in.ring, in.mask, tbi + (unsigned)pn) : SL::none();
+        pre = (has_in && pn < S2) ? SL::load(in.ring, in.mask, tbi + (unsigned)pn, in.sys) : SL::none();
         __syncwarp();
         if (has_in && lane == 0) st_ctr(in.cons, tbi + (unsigned)min(p0 + 32, S2));
         next_refill += P;
@@ -545,7 +575,7 @@ struct LongRunner {
         const int pr = pown & ((unsigned)gg < (unsigned)NT);
 #pragma unroll
         for (int k = 0; k < K; k += 2)
-          SL::put2(out.ring, out.mask, tbo + (unsigned)(K * gg + k), b[k], b[k + 1], pr);
+          SL::put2(out.ring, out.mask, tbo + (unsigned)(K * gg + k), b[k], b[k + 1], pr, out.sys);
       };
 #pragma unroll 1
       for (; t + 2 <= stop; t += 2, g += 2) {
@@ -700,9 +730,11 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
     const int k = pb.list[li];
     const int n0 = pb.lengths[k], m0 = pb.lengths[pb.num_pairs + k];
     int Rx;
-    if (choose_r(n0 < m0 ? n0 : m0, Rx)) continue;
+    if (choose_r(pb.shard ? pb.row_end - pb.row_begin : min(n0, m0), Rx)) continue;
+    // (+64: the producer's flow-control test looks up to 62 positions past the stream)
     const unsigned long long need_slots =
-        (unsigned long long)stream_len<C::F ? kLCols : 2>(min(n0, m0)) * Slots<T>::SPP;
+        (unsigned long long)(stream_len<C::F ? kLCols : 2>(pb.shard ? max(n0, m0) : min(n0, m0)) + 64) *
+        Slots<T>::SPP;
     unsigned long long cap = 2;
     while (cap < need_slots) cap <<= 1;
     if (cap <= pb.wrap_slots) wrap_mask = max(wrap_mask, (unsigned)(cap - 1ull));
@@ -710,7 +742,10 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
   if (wrap_mask)
     for (size_t i = (size_t)cta * blockDim.x + threadIdx.x; i <= (size_t)wrap_mask; i += (size_t)G * blockDim.x)
       pb.wrap[i] = make_uint2(0u, 0u);
-  if (cta == 0 && threadIdx.x == 0) pb.gcons[G] = 0u;
+  if (cta == 0 && threadIdx.x == 0) {
+    pb.gcons[G] = 0u;
+    if (pb.shard) pb.ext_cons[1] = pb.ext_out_tb;  // the next GPU's ring never needs flow control
+  }
   if constexpr (!TIER64) {
     for (int i = cta * (int)blockDim.x + (int)threadIdx.x; i < npairs; i += G * (int)blockDim.x) pb.bad[i] = 0;
     if (cta == 0 && threadIdx.x == 0) *pb.abort = 0;
@@ -756,8 +791,10 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
     int R;
     // one pass: the shorter curve on the rows; multi-pass: the longer one (the
     // wrap link then buffers the shorter curve's stream)
-    const bool multi = !choose_r(n0 < m0 ? n0 : m0, R);
-    const bool swap = multi ? n0 < m0 : n0 > m0;
+    // shard: the shorter curve on the rows always (every GPU must agree), its
+    // rows [row_begin, row_end) here
+    const bool multi = !choose_r(pb.shard ? pb.row_end - pb.row_begin : (n0 < m0 ? n0 : m0), R);
+    const bool swap = (multi && !pb.shard) ? n0 < m0 : n0 > m0;
     const int n = swap ? m0 : n0, m = swap ? n0 : m0;
     const In* rows = reinterpret_cast<const In*>(swap ? pb.q : pb.p) +
                      (swap ? pb.offsets[B + k] : pb.offsets[k]) * D;
@@ -765,7 +802,7 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
                      (swap ? pb.offsets[k] : pb.offsets[B + k]) * D;
     constexpr int KC = TIER64 ? 2 : kLCols;  // columns per step of this instantiation
     const unsigned S = (unsigned)stream_len<KC>(m);  // stream positions of this pair (see run_band)
-    if (multi && (unsigned long long)S * Slots<T>::SPP > (unsigned long long)wrap_mask + 1ull) {
+    if (multi && (unsigned long long)(S + 64) * Slots<T>::SPP > (unsigned long long)wrap_mask + 1ull) {
       // the wrap ring cannot buffer this stream (both curves longer than the
       // band scratch holds: > 16M points, int64 tier 8M): documented limit, no plausible value
       if (local == 0 && threadIdx.x == 0) {
@@ -775,10 +812,13 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
       continue;
     }
     const int band_rows = kWarp * R;
-    const int nb = (n + band_rows - 1) / band_rows;
+    const int rb = pb.shard ? pb.row_begin : 0, re = pb.shard ? pb.row_end : n;  // rows of this launch
+    const int nb = (re - rb + band_rows - 1) / band_rows;
     const int passes = (nb + NBP - 1) / NBP;
     const Link lin = (multi && j == 0) ? wrapL : in;
     const Link lout = (multi && j == NBP - 1) ? wrapL : out;
+    const Link ext_in{pb.ext_in, pb.ext_in_mask, pb.ext_cons, 1};
+    const Link ext_out{pb.ext_out, pb.ext_out_mask, pb.ext_cons + 1, 1};
     for (int pass = 0; pass < passes; pass++) {
       const int b = pass * NBP + j;  // band of this slot in this pass
       if (!(b < nb && b > 0) && lane == 0) {
@@ -788,11 +828,15 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
         st_ctr(lin.cons, tb + S);
       }
       if (b < nb) {
-        const bool has_in = b > 0, has_out = b + 1 < nb;
+        // the shard's first / last band link to the neighbouring GPUs
+        const bool x_in = b == 0 && rb > 0, x_out = b + 1 == nb && re < n;
+        const bool has_in = b > 0 || x_in, has_out = b + 1 < nb || x_out;
         // the wrap link's stream belongs to the next pass (its consumer, slot 0, reads it then)
-        const unsigned tbo = (j == NBP - 1) ? tb + S : tb;
+        const unsigned tbo = x_out ? pb.ext_out_tb : (j == NBP - 1) ? tb + S : tb;
+        const unsigned tbi = x_in ? pb.ext_in_tb : tb;
+        const Link lin_b = x_in ? ext_in : lin, lout_b = x_out ? ext_out : lout;
         auto go = [&](auto& run) {
-          run.n = n;
+          run.n = re;  // rows past the shard repeat its last row: exact for δ_dF (PAPER L259 footnote)
           run.m = m;
           run.rows = rows;
           run.cols = cols;
@@ -802,8 +846,8 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
           }
           const unsigned long long t0 = pb.trace ? gtimer() : 0ull;
           // fp32: four columns per step; int64 tier: two (its 64-bit state doubles the registers)
-          run.template run_band<KC>(b * band_rows, has_in, lin, tb, has_out, lout, tbo,
-                                                     b == nb - 1, k, pb.bad + li);
+          run.template run_band<KC>(rb + b * band_rows, has_in, lin_b, tbi, has_out, lout_b, tbo,
+                                    b == nb - 1 && re == n, k, pb.bad + li);
           if (pb.trace && lane == 0)
             printf("ffdtrace band %d cta %d warp %d start %llu end %llu\n", b, cta, warp, t0, gtimer());
         };
@@ -876,6 +920,16 @@ cudaError_t launch_long_k(const LongArgs& a, int sms, cudaStream_t st, const Lon
   LongProblem pb{a.p,     a.q,     a.offsets, a.lengths,  a.num_pairs, a.list, a.list_count, a.out,
                  w.gring, w.gcons, reinterpret_cast<uint2*>(a.wrap), wrap_slots, w.bad, w.abort, trace,
                  force_r};
+  pb.shard = a.shard;
+  pb.row_begin = a.row_begin;
+  pb.row_end = a.row_end;
+  pb.ext_in = reinterpret_cast<uint2*>(a.ext_in);
+  pb.ext_in_mask = a.ext_in_slots ? (unsigned)(a.ext_in_slots - 1) : 0u;
+  pb.ext_in_tb = a.ext_in_tb;
+  pb.ext_out = reinterpret_cast<uint2*>(a.ext_out);
+  pb.ext_out_mask = a.ext_out_slots ? (unsigned)(a.ext_out_slots - 1) : 0u;
+  pb.ext_out_tb = a.ext_out_tb;
+  pb.ext_cons = a.ext_cons;
   void* args[] = {&pb};
   // cluster size: the largest of 8/4/2 whose clusters can all be co-resident
   // for the whole grid (a smaller grid forces taller bands); FFD_LONG_CLUSTER=c

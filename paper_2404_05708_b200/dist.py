@@ -217,3 +217,75 @@ def cdist_self(A, norm: str = "l2", group=None, distribution: str = "p2p"):
             ffd.cdist_to(A, A[r1:], ptrs, n, norm=norm, rows=(r0, r1), col_offset=r1, mirror=True)
     hdl.barrier()
     return full
+
+
+# ---------------------------------------------------------------------------
+# One very long pair over W GPUs.  The long-pair wavefront is a
+# chain of row bands (linear memory); the chain simply continues
+# across GPUs.  Rank r computes a contiguous range of rows of the rows curve (the
+# shorter one) with ffd_long_pair_shard; its last band stores its bottom row,
+# slot by slot, straight into the next rank's ring in symmetric memory (NVLink
+# peer stores), where that rank's first band polls it.  A ring holds a whole
+# stream, so no rank ever waits for its consumer; the result is written by the
+# rank that holds the last row and broadcast.  Bit-identical to one GPU (the DP
+# only selects values; the bands and their inputs are the same).
+# ---------------------------------------------------------------------------
+def long_pair_row_ranges(rows: int, world: int, align: int) -> list[tuple[int, int]]:
+    """Contiguous row ranges [r0, r1) covering [0, rows), boundaries at multiples of
+    `align`, balanced; ranks beyond ⌈rows / align⌉ get an empty range at the end."""
+    if world < 1 or rows < 1 or align < 1:
+        raise ValueError("bad long_pair_row_ranges arguments")
+    active = min(world, -(-rows // align))
+    bounds = [min(rows, round(r * rows / active / align) * align) for r in range(active)] + [rows]
+    ranges = [(bounds[r], bounds[r + 1]) for r in range(active)]
+    return ranges + [(rows, rows)] * (world - active)
+
+
+_LONG_RINGS: dict = {}
+
+
+def long_pair(p, q, norm: str = "l2", group=None):
+    """δ_dF of ONE pair (p [n, dim], q [m, dim] fp32 CUDA tensors, identical on every
+    rank) with its rows split over the ranks of `group`.  Returns float32[1] on
+    every rank."""
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm_mem
+
+    import paper_2404_05708_b200 as ffd
+
+    n, m = p.shape[0], q.shape[0]
+    if group is None and not (dist.is_available() and dist.is_initialized()):
+        off = torch.zeros(2, dtype=torch.int64, device=p.device)
+        lens = torch.tensor([n, m], dtype=torch.int32, device=p.device)
+        return ffd.batch(p, q, off, lens, norm=norm)
+    pg = group if group is not None else dist.group.WORLD
+    world, rank = dist.get_world_size(pg), dist.get_rank(pg)
+    rows = min(n, m)
+    ranges = long_pair_row_ranges(rows, world, ffd.long_pair_row_align())
+    nbytes = ffd.long_pair_ring_bytes(n, m)
+    key = (nbytes, str(p.device), id(pg))
+    ent = _LONG_RINGS.get(key)
+    if ent is None:
+        ring = symm_mem.empty(nbytes, dtype=torch.uint8, device=p.device)
+        ring.zero_()
+        hdl = symm_mem.rendezvous(ring, pg)
+        ent = _LONG_RINGS[key] = {"ring": ring, "hdl": hdl, "tag": 0,
+                                  "ptrs": [int(hdl.buffer_ptrs[r]) for r in range(world)]}
+    slots = nbytes // 8
+    if ent["tag"] + 2 * slots >= 2 ** 32:  # tags are 32-bit: start over on zeroed rings
+        ent["hdl"].barrier()
+        ent["ring"].zero_()
+        ent["tag"] = 0
+    tag = ent["tag"]
+    ent["tag"] += slots
+    out = torch.full((1,), float("nan"), dtype=torch.float32, device=p.device)
+    ent["hdl"].barrier()  # every rank is done reading its ring from the previous call
+    r0, r1 = ranges[rank]
+    if r1 > r0:
+        nxt = (ent["ptrs"][rank + 1], nbytes) if r1 < rows else None
+        ffd.long_pair_shard(p, q, (r0, r1), norm, in_ring=ent["ring"] if r0 > 0 else None, in_tag=tag,
+                            out_ring=nxt, out_tag=tag, out=out)
+    last = max(r for r in range(world) if ranges[r][1] == rows and ranges[r][1] > ranges[r][0])
+    dist.broadcast(out, src=dist.get_global_rank(pg, last) if group is not None else last, group=group)
+    return out

@@ -205,3 +205,20 @@ def test_gloo_product_cdist(world, kind):
         p.join(180)
         assert p.exitcode == 0
     assert all(q.get(timeout=10) is True for _ in range(world))
+
+
+def test_long_pair_row_ranges():
+    from paper_2404_05708_b200.dist import long_pair_row_ranges
+    for rows in (1, 511, 512, 513, 20000, 262144, 1250000):
+        for w in (1, 2, 3, 4, 8):
+            rs = long_pair_row_ranges(rows, w, 512)
+            assert len(rs) == w and rs[0][0] == 0
+            covered = [x for r0, r1 in rs for x in (r0, r1) if r1 > r0]
+            assert all(rs[i][1] == rs[i + 1][0] for i in range(w - 1))
+            assert rs[-1][1] == rows
+            for r0, r1 in rs:
+                assert r1 >= r0
+                if r1 > r0:
+                    assert r0 % 512 == 0 and (r1 == rows or r1 % 512 == 0)
+            sizes = [r1 - r0 for r0, r1 in rs if r1 > r0]
+            assert covered and max(sizes) - min(sizes) <= 1024 or len(sizes) == 1

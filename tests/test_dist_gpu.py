@@ -132,3 +132,65 @@ def test_dist_product_over_nccl(ffd, nccl_group, distribution, kind):
     assert torch.equal(selfm, ffd.cdist_self(A, norm=norm))
     blk, rows = fdist.cdist(A, B, norm=norm, return_block=True)
     assert rows == (0, A.shape[0]) and torch.equal(blk, full)
+
+
+@pytest.mark.parametrize("W", [2, 3, 8])
+def test_long_pair_shards_emulated(ffd, W):
+    """ffd_long_pair_shard over W emulated GPUs, run one after another on this GPU
+    (the rings hold a whole stream, so no range waits for its consumer): the band
+    chain crosses the ranges through the rings and the result is bit-identical to
+    the single-call long-pair kernel, for two calls with the tag base advanced
+    (no re-zeroing) and with the ranges forced into several passes (1 CTA)."""
+    from paper_2404_05708_b200.dist import long_pair_row_ranges
+    rng = np.random.default_rng(40 + W)
+    n, m = 20000, 21001
+    p = torch.from_numpy(np.cumsum(rng.normal(size=(n, 2)), 0).astype(np.float32)).cuda()
+    q = torch.from_numpy(np.cumsum(rng.normal(size=(m, 2)), 0).astype(np.float32)).cuda()
+    off = torch.zeros(2, dtype=torch.int64, device="cuda")
+    lens = torch.tensor([n, m], dtype=torch.int32, device="cuda")
+    nbytes = ffd.long_pair_ring_bytes(n, m)
+    rings = [torch.zeros(nbytes, dtype=torch.uint8, device="cuda") for _ in range(W)]
+    ranges = long_pair_row_ranges(min(n, m), W, ffd.long_pair_row_align())
+    for norm in ("l2", "linf"):
+        full = ffd.batch(p, q, off, lens, norm=norm).item()
+        for call, ctas in enumerate(("", "", "1")):
+            if ctas:
+                os.environ["FFD_LONG_CTAS"] = ctas
+            try:
+                tag = (call + (norm == "linf") * 3) * (nbytes // 8)
+                out = torch.full((1,), float("nan"), device="cuda")
+                for r, (r0, r1) in enumerate(ranges):
+                    if r1 == r0:
+                        continue
+                    nxt = (rings[r + 1].data_ptr(), nbytes) if r1 < min(n, m) else None
+                    ffd.long_pair_shard(p, q, (r0, r1), norm, in_ring=rings[r] if r0 > 0 else None, in_tag=tag,
+                                        out_ring=nxt, out_tag=tag, out=out)
+            finally:
+                os.environ.pop("FFD_LONG_CTAS", None)
+            assert out.item() == full, (W, norm, call, out.item(), full)
+
+
+def test_long_pair_over_nccl(ffd, nccl_group):
+    """dist.long_pair through a real process group (world size 1: one range) and
+    its symmetric-memory ring, against the single-GPU call."""
+    from paper_2404_05708_b200 import dist as fdist
+    rng = np.random.default_rng(44)
+    p = torch.from_numpy(np.cumsum(rng.normal(size=(5000, 2)), 0).astype(np.float32)).cuda()
+    q = torch.from_numpy(np.cumsum(rng.normal(size=(7000, 2)), 0).astype(np.float32)).cuda()
+    off = torch.zeros(2, dtype=torch.int64, device="cuda")
+    lens = torch.tensor([5000, 7000], dtype=torch.int32, device="cuda")
+    for _ in range(2):
+        got = fdist.long_pair(p, q, "l1").item()
+        assert got == ffd.batch(p, q, off, lens, norm="l1").item()
+
+
+def test_long_pair_shard_rejects_bad_ranges(ffd):
+    p = torch.zeros((2000, 2), device="cuda")
+    q = torch.zeros((3000, 2), device="cuda")
+    ring = torch.zeros(ffd.long_pair_ring_bytes(2000, 3000), dtype=torch.uint8, device="cuda")
+    with pytest.raises(ffd.FFDError):
+        ffd.long_pair_shard(p, q, (100, 2000), in_ring=ring)              # unaligned begin
+    with pytest.raises(ffd.FFDError):
+        ffd.long_pair_shard(p, q, (0, 1000))                              # no out ring
+    with pytest.raises(ffd.FFDError):
+        ffd.long_pair_shard(p, q, (512, 2000))                            # no in ring

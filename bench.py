@@ -681,6 +681,31 @@ def bench_long(args):
     e3.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e2.elapsed_time(e3) / args.steps
+    # N > 1: the same pair with its rows split over the ranks (SURVEY §8(f) f4,
+    # dist.long_pair: the band chain continues across GPUs through NVLink rings)
+    sharded = None
+    if ws > 1:
+        from paper_2404_05708_b200 import dist as fdist
+        try:
+            for nm in cfg.norms:
+                fdist.long_pair(p, q, nm)
+            torch.cuda.synchronize()
+            dist.barrier()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            for _ in range(args.steps):
+                res = {nm: fdist.long_pair(p, q, nm) for nm in cfg.norms}
+            s1.record(stream)
+            torch.cuda.synchronize()
+            t = torch.tensor([s0.elapsed_time(s1) / args.steps], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            sh_ms = float(t[0])
+            sharded = {"value": 3 * cells / (sh_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": sh_ms,
+                       "scaling": "strong", "matches_one_gpu": all(float(res[nm].item()) == float(outs[nm].item())
+                                                                   for nm in cfg.norms),
+                       "api": "dist.long_pair: rows split over the ranks, ffd_long_pair_shard, symmetric-memory rings"}
+        except Exception as e:  # reported, never silently replaced
+            sharded = {"error": f"{type(e).__name__}: {e}"[:300]}
     if rank == 0:
         clocks = sampler.summary()
         f_max = (clocks["sm_max_mhz"] or SM_MAX_MHZ_NOMINAL) * 1e6
@@ -706,6 +731,7 @@ def bench_long(args):
             "e2e": {"value": ws * 3 * cells / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": p_h.nbytes + q_h.nbytes, "d2h_bytes_per_step": 4 * len(cfg.norms)},
             "results": vals,
+            "sharded_one_pair": sharded,
             "gpu_launches": launches * args.steps, "gpu_launches_per_step": launches,
         }
         print(json.dumps(line), flush=True)

@@ -210,10 +210,189 @@ __global__ void __launch_bounds__(kWarp* kWarpsPerCta, (R > 16) ? 3 : kCdMinCtas
   if (pb.dst.n > 1) __threadfence_system();
 }
 
+// ---- two columns per step ------------------------------------------------------
+// The same work items with each segment lane processing positions 2(t−s) and
+// 2(t−s)+1 per step (strip.cuh step2_compute): the second column's min/max chain
+// trails the first by one row, so the two chains interleave and the shuffle +
+// chain latency is paid once per two columns.  Every B curve's stream segment
+// is padded to an even period P2 = sentinel + lenB columns (+ one more copy of
+// the last column when lenB + 1 is odd: a repeated point leaves δ unchanged,
+// PAPER L259 footnote), so a sentinel is always a step's first column and a
+// curve's last column a step's second: the corner value and the result need no
+// per-column case.  Unlike the batch kernel there are no transition windows
+// (the A curve of a segment is fixed for the item), so nothing pays for the
+// longer step.
+template <int KIND, int D, int W, int R, int FIN>
+__global__ void __launch_bounds__(kWarp* kWarpsPerCta, (R > 16) ? 3 : kCdMinCtasPerSm)
+    cdist_kernel2(const CdistProblem pb) {
+  using C = SCfg<float, KIND, D, false>;
+  static_assert(!C::XSQ, "cdist: fp32 inputs");
+  constexpr int SEG = kWarp / W;
+  constexpr int EW = C::EW;
+  __shared__ uint4 ring_all[kWarpsPerCta][kRing * EW];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = lane % W;        // lane index inside the segment
+  const int seg = lane / W;      // segment index inside the warp
+  uint4* ring = ring_all[warp];
+  const int P2 = (pb.lenB + 2) & ~1;  // even stream period
+  const int H = P2 >> 1;              // steps per period
+
+  while (true) {
+    int64_t item = 0;
+    if (lane == 0) item = atomicAdd(pb.counter, 1);
+    item = __shfl_sync(0xffffffffu, (long long)item, 0);
+    if (item >= pb.n_items) break;
+    const int64_t ablk = item / pb.tiles_b;
+    const int64_t tb = item % pb.tiles_b;
+    const int64_t a = pb.row_begin + ablk * SEG + seg;
+    const bool a_ok = a < pb.row_end;
+    const int64_t b0 = tb * kCdTile;
+    const int nb = (int)min((int64_t)kCdTile, pb.nB - b0);
+    if (pb.self) {
+      const int64_t a_first = pb.row_begin + ablk * SEG;
+      const int64_t bb0 = pb.dst.col_off + b0;
+      if (bb0 + nb <= a_first && bb0 >= pb.row_begin) continue;
+    }
+    const int S = nb * P2 + 2;  // positions: the periods, then a final sentinel and one more
+
+    float x[C::NS][R];
+    {
+      const float* ap = pb.A + (a_ok ? a : pb.row_begin) * (int64_t)pb.lenA * D;
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        const int row = min(s * R + r, pb.lenA - 1);
+#pragma unroll
+        for (int c = 0; c < D; c++) x[c][r] = __ldg(ap + (int64_t)row * D + c);
+      }
+    }
+    const float* bbase = pb.B + b0 * (int64_t)pb.lenB * D;
+    auto load_pt = [&](int pos, float (&v)[D]) {
+      const int b = pos / P2, k = pos - b * P2;
+      if (pos < S - 2 && k != 0) {
+        const float* bp = bbase + ((int64_t)b * pb.lenB + min(k - 1, pb.lenB - 1)) * D;
+#pragma unroll
+        for (int c = 0; c < D; c++) v[c] = __ldg(bp + c);
+      } else {
+#pragma unroll
+        for (int c = 0; c < D; c++) v[c] = finf();
+      }
+    };
+    auto store_el = [&](int pos, const float (&v)[D]) {
+      alignas(16) float e[C::EBYTES / 4];
+#pragma unroll
+      for (int i = 0; i < C::EBYTES / 4; i++) e[i] = 0.f;
+#pragma unroll
+      for (int c = 0; c < D; c++) e[c] = v[c];
+      uint4* dst = ring + (pos & kRingMask) * EW;
+#pragma unroll
+      for (int w = 0; w < EW; w++) dst[w] = reinterpret_cast<const uint4*>(e)[w];
+    };
+    float pre[D];
+    {
+      float v0[D];
+      load_pt(lane, v0);
+      store_el(lane, v0);
+      load_pt(32 + lane, pre);
+    }
+    __syncwarp();
+
+    float c[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) c[r] = finf();
+    float diag = finf(), b0v = finf();
+    // one step on positions 2g, 2g+1; `top0` is what the segment's first lane sees
+    // above its first row in the first column: the corner 0 on a sentinel (t ≡ 0
+    // mod H), +∞ otherwise (the second column is never a sentinel)
+    auto step = [&](int t, float top0) {
+      const int g = t - s;
+      alignas(16) float e0[C::EBYTES / 4], e1[C::EBYTES / 4];
+      {
+        const uint4* src = ring + ((2 * g) & kRingMask) * EW;
+#pragma unroll
+        for (int w = 0; w < EW; w++) {
+          reinterpret_cast<uint4*>(e0)[w] = src[w];
+          reinterpret_cast<uint4*>(e1)[w] = src[EW + w];
+        }
+      }
+      const float upv0 = __shfl_up_sync(0xffffffffu, b0v, 1, W);
+      const float upv1 = __shfl_up_sync(0xffffffffu, c[R - 1], 1, W);
+      const float up0 = (s == 0) ? top0 : upv0;
+      const float up1 = (s == 0) ? finf() : upv1;
+      float d0[R], d1[R];
+      cell_dists<float, KIND, D, R, false>(x, e0, d0);
+      cell_dists<float, KIND, D, R, false>(x, e1, d1);
+      {
+        float u = up0, dg = diag;
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+          const float nv = fmaxf(fminf(fminf(u, dg), c[r]), d0[r]);
+          dg = c[r];
+          c[r] = nv;
+          u = nv;
+        }
+      }
+      b0v = c[R - 1];
+      {
+        float u = up1, dg = up0;
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+          const float nv = fmaxf(fminf(fminf(u, dg), c[r]), d1[r]);
+          dg = c[r];
+          c[r] = nv;
+          u = nv;
+        }
+      }
+      diag = up1;
+    };
+    const int total = (S >> 1) + W - 1;
+    int next_out = H + W - 1;  // segment-last lanes have finished B curve out_b (after step next_out − 1)
+    int out_b = 0;
+    int next_refill = 16;      // 32 positions per refill
+    int next_sent = 0;         // segment-first lanes on a sentinel step
+    int t = 0;
+    while (t < total) {
+      const int stop = min(min(min(next_refill, next_out), next_sent), total);
+#pragma unroll 2
+      for (; t < stop; ++t) step(t, finf());
+      if (t >= total) break;
+      if (t == next_refill) {
+        store_el(2 * t + lane, pre);
+        load_pt(2 * t + 32 + lane, pre);
+        next_refill += 16;
+        __syncwarp();
+      }
+      if (t == next_out) {
+        if (s == W - 1 && a_ok && out_b < nb) {
+          float v = c[R - 1];
+          if constexpr (FIN == F_SQRT) v = __fsqrt_rn(v);
+          const int64_t b = pb.dst.col_off + b0 + out_b;
+          const bool in_shard = pb.self && b >= pb.row_begin && b < pb.row_end;
+          if (!(in_shard && b < a)) put_result(pb.dst, a, b, v);
+          if ((in_shard && b > a) || (pb.dst.mirror && !pb.self)) put_result(pb.dst, b, a, v);
+        }
+        ++out_b;
+        next_out += H;
+      }
+      if (t == next_sent) {
+        step(t, 0.f);
+        ++t;
+        next_sent += H;
+      }
+    }
+    __syncwarp();
+  }
+  if (pb.dst.n > 1) __threadfence_system();
+}
+
 // ---- dispatch ----------------------------------------------------------------
+#ifndef FFD_CDIST_COLS
+#define FFD_CDIST_COLS 2
+#endif
 template <int KIND, int D, int W, int R, int FIN>
 static cudaError_t launch_one(const CdistProblem& pb, int sms, cudaStream_t st) {
-  auto k = cdist_kernel<KIND, D, W, R, FIN>;
+  // columns per step: FFD_CDIST_COLS at build time, overridable by the environment (testing)
+  static const int cols = getenv("FFD_CDIST_COLS") ? atoi(getenv("FFD_CDIST_COLS")) : FFD_CDIST_COLS;
+  auto k = cols == 2 ? cdist_kernel2<KIND, D, W, R, FIN> : cdist_kernel<KIND, D, W, R, FIN>;
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kWarp * kWarpsPerCta, 0);
   if (occ < 1) occ = 1;

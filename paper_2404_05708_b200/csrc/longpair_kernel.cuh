@@ -456,7 +456,10 @@ struct LongRunner {
 
   // one band of 32·R rows starting at row r0, K columns per warp step (PipeK).
   // tbi / tbo: tag bases of the input / output link streams.
-  template <int K>
+  // SYS: the band has a cross-GPU link (ffd_long_pair_shard): its per-step slot
+  // accesses use system scope (a compile-time choice: a runtime branch in the
+  // per-step store cost config 5 15 %)
+  template <int K, bool SYS>
   __device__ bool run_band(int r0, bool has_in, Link in, unsigned tbi, bool has_out, Link out,
                            unsigned tbo, bool last_band, int out_idx, int* bad_flag) {
     static_assert(K == 2 || K == 4, "K columns per step");
@@ -497,11 +500,11 @@ struct LongRunner {
     int kind, kind2;
     fetch(lane, S2, lead, a, kind);
     wait_chunk(31, S2, has_in, in, tbi);
-    Pre pre = (has_in && lane < S2) ? SL::load(in.ring, in.mask, tbi + (unsigned)lane, in.sys) : SL::none();
+    Pre pre = (has_in && lane < S2) ? SL::load(in.ring, in.mask, tbi + (unsigned)lane, SYS) : SL::none();
     store_elem<K>(a, kind, lane, top_of(lane, S2, lead, has_in, in, tbi, pre), ok);
     fetch(32 + lane, S2, lead, a, kind);
     fetch(64 + lane, S2, lead, a2, kind2);
-    pre = (has_in && 32 + lane < S2) ? SL::load(in.ring, in.mask, tbi + (unsigned)(32 + lane), in.sys) : SL::none();
+    pre = (has_in && 32 + lane < S2) ? SL::load(in.ring, in.mask, tbi + (unsigned)(32 + lane), SYS) : SL::none();
     __syncwarp();
     if (has_in && lane == 0) st_ctr(in.cons, tbi + (unsigned)min(32, S2));
     const unsigned cap = (out.mask + 1u) / SL::SPP;  // output ring capacity in positions
@@ -534,7 +537,7 @@ struct LongRunner {
         kind = kind2;
         fetch(p0 + 64 + lane, S2, lead, a2, kind2);
         const int pn = p0 + 32 + lane;
-        pre = (has_in && pn < S2) ? SL::load(in.ring, in.mask, tbi + (unsigned)pn, in.sys) : SL::none();
+        pre = (has_in && pn < S2) ? SL::load(in.ring, in.mask, tbi + (unsigned)pn, SYS) : SL::none();
         __syncwarp();
         if (has_in && lane == 0) st_ctr(in.cons, tbi + (unsigned)min(p0 + 32, S2));
         next_refill += P;
@@ -575,7 +578,7 @@ struct LongRunner {
         const int pr = pown & ((unsigned)gg < (unsigned)NT);
 #pragma unroll
         for (int k = 0; k < K; k += 2)
-          SL::put2(out.ring, out.mask, tbo + (unsigned)(K * gg + k), b[k], b[k + 1], pr, out.sys);
+          SL::put2(out.ring, out.mask, tbo + (unsigned)(K * gg + k), b[k], b[k + 1], pr, SYS);
       };
 #pragma unroll 1
       for (; t + 2 <= stop; t += 2, g += 2) {
@@ -846,8 +849,12 @@ __global__ void __launch_bounds__(kWarp* kLWarps, 1) long_kernel(const LongProbl
           }
           const unsigned long long t0 = pb.trace ? gtimer() : 0ull;
           // fp32: four columns per step; int64 tier: two (its 64-bit state doubles the registers)
-          run.template run_band<KC>(rb + b * band_rows, has_in, lin_b, tbi, has_out, lout_b, tbo,
-                                    b == nb - 1 && re == n, k, pb.bad + li);
+          if (x_in || x_out)
+            run.template run_band<KC, true>(rb + b * band_rows, has_in, lin_b, tbi, has_out, lout_b, tbo,
+                                            b == nb - 1 && re == n, k, pb.bad + li);
+          else
+            run.template run_band<KC, false>(rb + b * band_rows, has_in, lin_b, tbi, has_out, lout_b, tbo,
+                                             b == nb - 1 && re == n, k, pb.bad + li);
           if (pb.trace && lane == 0)
             printf("ffdtrace band %d cta %d warp %d start %llu end %llu\n", b, cta, warp, t0, gtimer());
         };

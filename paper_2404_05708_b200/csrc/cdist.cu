@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(kWarp* kWarpsPerCta, (R > 16) ? 3 : kCdMinCtas
         // segment-last lanes hold δ(A_a, B_{b0+out_b}): column P·(out_b+1) − 1 is done
         if (s == W - 1 && a_ok) {
           float v = c[R - 1];
-          if constexpr (FIN == F_SQRT) v = __fsqrt_rn(v);
+          if constexpr (FIN == F_SQRT) v = sqrt_result(v);
           const int64_t b = pb.dst.col_off + b0 + out_b;  // column of the result
           const bool in_shard = pb.self && b >= pb.row_begin && b < pb.row_end;
           // self mode: (a, b) with b < a inside the shard is the mirror's job
@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(kWarp* kWarpsPerCta, (R > 16) ? 3 : kCdMinCtas
       if (t == next_out) {
         if (s == W - 1 && a_ok && out_b < nb) {
           float v = c[R - 1];
-          if constexpr (FIN == F_SQRT) v = __fsqrt_rn(v);
+          if constexpr (FIN == F_SQRT) v = sqrt_result(v);
           const int64_t b = pb.dst.col_off + b0 + out_b;
           const bool in_shard = pb.self && b >= pb.row_begin && b < pb.row_end;
           if (!(in_shard && b < a)) put_result(pb.dst, a, b, v);

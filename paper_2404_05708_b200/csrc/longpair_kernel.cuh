@@ -612,7 +612,7 @@ struct LongRunner {
         reinterpret_cast<long long*>(pb.out)[out_idx] = bad ? LLONG_MIN : (long long)c[R - 1];
       } else {
         float f = c[R - 1];
-        if constexpr (FIN == F_SQRT) f = __fsqrt_rn(f);
+        if constexpr (FIN == F_SQRT) f = sqrt_result(f);
         reinterpret_cast<float*>(pb.out)[out_idx] = dead ? __int_as_float(0x7fc00000) : f;
       }
     }

@@ -252,7 +252,7 @@ __device__ __forceinline__ int lring(int p) {
 // (r, k) needs (r, k−1) and (r−1, k)), so the K chains interleave and the
 // shuffle + chain latency is paid once per K columns.  Lane ℓ hands lane ℓ+1 its
 // bottom value after each of the K columns (K shuffles per step).  Software-
-// pipelined like strip.cuh Pipe2: the distances of step g+1 are computed during
+// pipelined: the distances of step g+1 are computed during
 // step g's chains and the ring elements of step g+2 are loaded.
 template <typename T, int KIND, int D, int R, bool INT_IN, int K, bool DTW = false>
 struct PipeK {

@@ -251,3 +251,21 @@ def test_small_batch_multiband_pairs_on_groups(ffd):
     pairs += [(walk(rng, int(rng.integers(513, 3000))), walk(rng, int(rng.integers(513, 3000)))) for _ in range(20)]
     pairs += [(walk(rng, 300), walk(rng, 2000)), (walk(rng, 40), walk(rng, 30))]
     _check_mirror_batch(run_pairs(ffd, pairs, "l2"), pairs, "l2")
+
+
+def test_int64_tier_multipass(ffd):
+    """An int32 pair outside the fp32-exact window on 1–2 CTAs: the exact int64
+    tier runs it in several passes through the wrap link (64-bit values travel
+    as two tagged slots), bit-exact; with an in-window pair beside it."""
+    rng = np.random.default_rng(12)
+    pairs = [(rng.integers(-20000, 20001, size=(9000, 2)).astype(np.int32),
+              rng.integers(-20000, 20001, size=(8700, 2)).astype(np.int32)),
+             (walk(rng, 6000, kind="i"), walk(rng, 6500, kind="i"))]
+    exp = [oracle.pair(p, q, "sql2", form="linear") for p, q in pairs]
+    for ctas in ("1", "2"):
+        os.environ["FFD_LONG_CTAS"] = ctas
+        try:
+            got = run_pairs(ffd, pairs, "sql2")
+        finally:
+            del os.environ["FFD_LONG_CTAS"]
+        assert list(got) == exp, (ctas, got, exp)

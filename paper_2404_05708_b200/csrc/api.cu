@@ -14,6 +14,7 @@
 #include "longpair.cuh"
 #include "prep.cuh"
 #include "registry.h"
+#include "seg.cuh"
 #include "strip.cuh"
 #include "validate.cuh"
 
@@ -102,8 +103,8 @@ static BatchWs batch_layout(void* base, int64_t B, int sms) {
     return p;
   };
   w.counters = reinterpret_cast<int*>(take(sizeof(int) * kNumCtr));
-  w.hist = reinterpret_cast<int*>(take(sizeof(int) * kNumKeys));
-  w.cursor = reinterpret_cast<int*>(take(sizeof(int) * kNumKeys));
+  w.hist = reinterpret_cast<int*>(take(sizeof(int) * kAllKeys));
+  w.cursor = reinterpret_cast<int*>(take(sizeof(int) * kAllKeys));
   w.tmp = reinterpret_cast<PairDesc*>(take(sizeof(PairDesc) * (size_t)B));
   w.sorted = reinterpret_cast<PairDesc*>(take(sizeof(PairDesc) * (size_t)B));
   w.keys = reinterpret_cast<int16_t*>(take(sizeof(int16_t) * (size_t)B));
@@ -113,6 +114,9 @@ static BatchWs batch_layout(void* base, int64_t B, int sms) {
   const size_t warps_fb = (size_t)sms * kCtasFb * kWarpsPerCta;
   w.scratch_main = reinterpret_cast<float*>(take(warps_main * 2 * kScratchCols * sizeof(float)));
   w.scratch_fb = reinterpret_cast<long long*>(take(warps_fb * 2 * kScratchCols * sizeof(long long)));
+  w.seg_sorted = reinterpret_cast<PairDesc*>(take(sizeof(PairDesc) * (size_t)B));
+  w.seg_items = take(sizeof(SegItem) * (size_t)seg_max_items(B));
+  w.seg_item_off = reinterpret_cast<int*>(take(sizeof(int) * kSegBins));
   w.bytes = off;
   return w;
 }
@@ -168,7 +172,9 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
   // (the fp64 DTW tier has no long-pair path: 0, such pairs get NaN)
   const int long_ok = measure == 0 ? medium_rows_for(B, di.sms) : measure == 2 ? 0 : (dtw_all_long ? -2 : -1);
   const int out_kind = int_in ? 1 : (measure == 2 ? 2 : 0);
-  if (launch_prep(offsets, lengths, B, out_kind, long_ok, out, ws, di.sms, st, &g_launches) !=
+  // single-band Fréchet pairs of the built cells go to the segmented kernel (seg.cuh)
+  const bool use_seg = measure == 0 && B > kPrepSmallMax && seg_supported(kind, dim, int_in, fin);
+  if (launch_prep(offsets, lengths, B, out_kind, long_ok, out, ws, di.sms, st, &g_launches, use_seg) !=
       cudaSuccess)
     return FFD_ERR_CUDA;
 
@@ -206,8 +212,22 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
     const int64_t need = (chunks + kWarpsPerCta - 1) / kWarpsPerCta;
     const int ctas = (int)(need < (int64_t)di.sms * occ ? need : (int64_t)di.sms * occ);
     if (main_e->launch(pb, ctas, st) != cudaSuccess) return FFD_ERR_CUDA;
+    ++g_launches;
+    if (use_seg) {
+      SegProblem sp{};
+      sp.p = p;
+      sp.q = q;
+      sp.sorted = ws.seg_sorted;
+      sp.items = reinterpret_cast<const SegItem*>(ws.seg_items);
+      sp.n_items = ws.counters + kCtrSegItems;
+      sp.counter = ws.counters + kCtrSegChunk;
+      sp.out = out;
+      sp.fb_list = ws.fb_list;
+      sp.fb_count = ws.counters + kCtrFb;
+      if (launch_seg(sp, kind, dim, int_in, fin, di.sms, st) != cudaSuccess) return FFD_ERR_CUDA;
+      ++g_launches;
+    }
   }
-  ++g_launches;
 
   if (fb_e) {
     Problem fb = pb;

@@ -7,6 +7,7 @@
 // < 1 get their invalid-output value here and are dropped; pairs too long for
 // the batch kernel's band scratch go to the long-pair list.
 #include "prep.cuh"
+#include "seg.cuh"
 
 namespace ffd {
 
@@ -23,11 +24,31 @@ __device__ __forceinline__ void write_invalid(void* out, int64_t k, int out_kind
 __device__ __forceinline__ int pair_key(const int64_t* __restrict__ offsets,
                                         const int32_t* __restrict__ lengths, int64_t B, int64_t k,
                                         int int_out, int long_ok, void* __restrict__ out, PairDesc& d,
-                                        int* __restrict__ long_list, int* __restrict__ long_count) {
+                                        int* __restrict__ long_list, int* __restrict__ long_count,
+                                        bool seg = false) {
   const int n = lengths[k], m = lengths[B + k];
   if (n < 1 || m < 1) {
     write_invalid(out, k, int_out);
     return -1;
+  }
+  if (seg && long_ok > 0) {
+    // the segmented kernel (seg.cuh): single-band Fréchet pairs, the longer curve on the rows
+    const int bin = seg_bin(n, m);
+    if (bin >= 0) {
+      int W, R;
+      seg_shape(bin / kSegHB, W, R);
+      const bool swap = n < m;
+      d.row_off = swap ? offsets[B + k] : offsets[k];
+      d.col_off = swap ? offsets[k] : offsets[B + k];
+      d.n_rows = swap ? m : n;
+      d.m_cols = swap ? n : m;
+      d.idx = (int)k;
+      d.R = (uint8_t)R;
+      d.nb = 1;
+      d.swap = swap;
+      d.pad = 0;
+      return kNumKeys + bin;
+    }
   }
   // Orientation: the rows (held in registers, R per lane) are the shorter curve,
   // unless a Fréchet pair is estimated cheaper with the LONGER curve as rows —
@@ -78,14 +99,15 @@ __global__ void prep_keys_kernel(const int64_t* __restrict__ offsets,
                                  const int32_t* __restrict__ lengths, int64_t B, int int_out, int long_ok,
                                  void* __restrict__ out, PairDesc* __restrict__ tmp,
                                  int16_t* __restrict__ keys, int* __restrict__ hist,
-                                 int* __restrict__ long_list, int* __restrict__ long_count) {
-  __shared__ int h[kNumKeys];
-  for (int i = threadIdx.x; i < kNumKeys; i += blockDim.x) h[i] = 0;
+                                 int* __restrict__ long_list, int* __restrict__ long_count, int seg) {
+  __shared__ int h[kAllKeys];
+  const int nk = seg ? kAllKeys : kNumKeys;
+  for (int i = threadIdx.x; i < nk; i += blockDim.x) h[i] = 0;
   __syncthreads();
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < B;
        k += (int64_t)gridDim.x * blockDim.x) {
     PairDesc d;
-    const int key = pair_key(offsets, lengths, B, k, int_out, long_ok, out, d, long_list, long_count);
+    const int key = pair_key(offsets, lengths, B, k, int_out, long_ok, out, d, long_list, long_count, seg != 0);
     if (key >= 0) {
       tmp[k] = d;
       atomicAdd(&h[key], 1);
@@ -93,7 +115,7 @@ __global__ void prep_keys_kernel(const int64_t* __restrict__ offsets,
     keys[k] = (int16_t)key;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < kNumKeys; i += blockDim.x)
+  for (int i = threadIdx.x; i < nk; i += blockDim.x)
     if (h[i]) atomicAdd(&hist[i], h[i]);
 }
 
@@ -176,7 +198,8 @@ __global__ void prep_scan_kernel(const int* __restrict__ hist, int* __restrict__
 
 __global__ void prep_scatter_kernel(const PairDesc* __restrict__ tmp,
                                     const int16_t* __restrict__ keys, int64_t B,
-                                    int* __restrict__ cursor, PairDesc* __restrict__ sorted) {
+                                    int* __restrict__ cursor, PairDesc* __restrict__ sorted,
+                                    PairDesc* __restrict__ seg_sorted) {
   // warp-aggregated: the lanes holding the same key take one atomicAdd for all
   // of them (a batch has only a handful of distinct shapes, so per-pair atomics
   // on one cursor serialise)
@@ -190,13 +213,105 @@ __global__ void prep_scatter_kernel(const PairDesc* __restrict__ tmp,
     int pos = 0;
     if (key >= 0 && lane == leader) pos = atomicAdd(&cursor[key], __popc(peers));
     pos = __shfl_sync(0xffffffffu, pos, leader);
-    if (key >= 0) sorted[pos + rank] = tmp[k];
+    if (key >= 0) (key >= kNumKeys ? seg_sorted : sorted)[pos + rank] = tmp[k];
+  }
+}
+
+
+// exclusive scan of a[0, n) in shared memory by every thread of the block; returns the total
+__device__ int block_scan_excl(int* a, int n) {
+  __shared__ int wsum[32];
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int P = (n + blockDim.x - 1) / blockDim.x, b = threadIdx.x * P;
+  int loc = 0;
+  for (int i = 0; i < P; i++)
+    if (b + i < n) loc += a[b + i];
+  int v = loc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += y;
+  }
+  if (lane == 31) wsum[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    int x = lane < nw ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    wsum[lane] = x;
+  }
+  __syncthreads();
+  int excl = v - loc + (w > 0 ? wsum[w - 1] : 0);
+  const int total = wsum[nw - 1];
+  for (int i = 0; i < P; i++)
+    if (b + i < n) {
+      const int t = a[b + i];
+      a[b + i] = excl;
+      excl += t;
+    }
+  __syncthreads();
+  return total;
+}
+
+// one block of 1024 threads: the batch kernel's bins (descending) as
+// prep_scan_kernel, then the segmented kernel's bins (descending: the largest
+// shape and period first) -> pair cursors, and its items (G·L pairs of one bin
+// each) -> first item per bin (in rank order) and the item count
+__global__ void __launch_bounds__(1024) prep_scan_seg_kernel(const int* __restrict__ hist, int* __restrict__ cursor,
+                                                             int* __restrict__ item_off, int* __restrict__ counters,
+                                                             int L) {
+  __shared__ int s[kSegBins];
+  for (int r = threadIdx.x; r < kNumKeys; r += blockDim.x) s[r] = hist[kNumKeys - 1 - r];
+  const int total = block_scan_excl(s, kNumKeys);
+  for (int r = threadIdx.x; r < kNumKeys; r += blockDim.x) cursor[kNumKeys - 1 - r] = s[r];
+  __syncthreads();
+  for (int r = threadIdx.x; r < kSegBins; r += blockDim.x) s[r] = hist[kNumKeys + kSegBins - 1 - r];
+  block_scan_excl(s, kSegBins);
+  for (int r = threadIdx.x; r < kSegBins; r += blockDim.x) cursor[kNumKeys + kSegBins - 1 - r] = s[r];
+  __syncthreads();
+  for (int r = threadIdx.x; r < kSegBins; r += blockDim.x) {
+    const int bin = kSegBins - 1 - r, cnt = hist[kNumKeys + bin], gl = seg_item_pairs(bin, L);
+    s[r] = (cnt + gl - 1) / gl;
+  }
+  const int items = block_scan_excl(s, kSegBins);
+  for (int r = threadIdx.x; r < kSegBins; r += blockDim.x) item_off[r] = s[r];
+  if (threadIdx.x == 0) {
+    counters[kCtrNumSorted] = total;
+    counters[kCtrSegItems] = items;
+  }
+}
+
+// item i -> (first pair, pairs, shape): the bin whose item range holds i
+__global__ void prep_seg_items_kernel(const int* __restrict__ hist, const int* __restrict__ cursor,
+                                      const int* __restrict__ item_off, const int* __restrict__ counters,
+                                      SegItem* __restrict__ items, int64_t max_items, int L) {
+  const int n = counters[kCtrSegItems];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n && i < max_items;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = kSegBins;  // first rank with item_off > i
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (item_off[mid] <= i) lo = mid + 1;
+      else hi = mid;
+    }
+    const int r = lo - 1, bin = kSegBins - 1 - r;
+    const int gl = seg_item_pairs(bin, L), local = (int)i - item_off[r];
+    const int cnt = hist[kNumKeys + bin];
+    SegItem it;
+    it.start = cursor[kNumKeys + bin] + local * gl;
+    it.count = (int16_t)min(gl, cnt - local * gl);
+    it.shape = (int16_t)(bin / kSegHB);
+    items[i] = it;
   }
 }
 
 cudaError_t launch_prep(const int64_t* offsets, const int32_t* lengths, int64_t B, int int_out,
                         int long_ok, void* out, const BatchWs& ws, int num_sms, cudaStream_t st,
-                        int64_t* launches) {
+                        int64_t* launches, bool seg) {
   if (B == 0) return cudaSuccess;
   if (B <= kPrepSmallMax) {
     prep_small_kernel<<<1, kPrepSmallThreads, 0, st>>>(offsets, lengths, B, int_out, long_ok, out,
@@ -213,10 +328,21 @@ cudaError_t launch_prep(const int64_t* offsets, const int32_t* lengths, int64_t 
   if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
   prep_keys_kernel<<<(int)blocks, threads, 0, st>>>(offsets, lengths, B, int_out, long_ok, out, ws.tmp,
                                                     ws.keys, ws.hist, ws.long_list,
-                                                    ws.counters + kCtrLong);
-  prep_scan_kernel<<<1, kNumKeys, 0, st>>>(ws.hist, ws.cursor, ws.counters + kCtrNumSorted);
-  prep_scatter_kernel<<<(int)blocks, threads, 0, st>>>(ws.tmp, ws.keys, B, ws.cursor, ws.sorted);
-  *launches += 3;
+                                                    ws.counters + kCtrLong, seg ? 1 : 0);
+  if (seg) {
+    const int L = seg_items_per_segment();
+    prep_scan_seg_kernel<<<1, 1024, 0, st>>>(ws.hist, ws.cursor, ws.seg_item_off, ws.counters, L);
+    const int64_t mi = seg_max_items(B);
+    const int ib = (int)((mi + 255) / 256 < (int64_t)num_sms * 4 ? (mi + 255) / 256 : (int64_t)num_sms * 4);
+    prep_seg_items_kernel<<<ib, 256, 0, st>>>(ws.hist, ws.cursor, ws.seg_item_off, ws.counters,
+                                              reinterpret_cast<SegItem*>(ws.seg_items), mi, L);
+    *launches += 2;
+  } else {
+    prep_scan_kernel<<<1, kNumKeys, 0, st>>>(ws.hist, ws.cursor, ws.counters + kCtrNumSorted);
+    *launches += 1;
+  }
+  prep_scatter_kernel<<<(int)blocks, threads, 0, st>>>(ws.tmp, ws.keys, B, ws.cursor, ws.sorted, ws.seg_sorted);
+  *launches += 2;
   return cudaGetLastError();
 }
 

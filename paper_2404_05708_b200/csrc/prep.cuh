@@ -8,7 +8,9 @@
 
 namespace ffd {
 
-constexpr int kNumKeys = kMaxBands * kMaxR;  // 256 shape bins
+constexpr int kNumKeys = kMaxBands * kMaxR;  // 256 shape bins of the batch kernel
+constexpr int kSegBinsP = 16 * 65;          // (shape, period) bins of the segmented kernel (seg.cuh kSegBins)
+constexpr int kAllKeys = kNumKeys + kSegBinsP;
 constexpr int64_t kPrepSmallMax = 4096;      // batches up to this size: one-block prep
 
 // a valid pair (n, m ≥ 1) too long for the batch kernel's bands / band scratch
@@ -47,6 +49,8 @@ enum : int {
   kCtrFb = 3,
   kCtrLong = 4,
   kCtrChunkLong = 5,
+  kCtrSegItems = 6,  // items of the segmented kernel
+  kCtrSegChunk = 7,  // its item pop counter
   kNumCtr = 8
 };
 
@@ -54,21 +58,26 @@ struct BatchWs {
   PairDesc* tmp;      // [B]
   PairDesc* sorted;   // [B]
   int16_t* keys;      // [B]
-  int* hist;          // [kNumKeys]
-  int* cursor;        // [kNumKeys]
+  int* hist;          // [kAllKeys]: batch-kernel shape bins, then segmented-kernel bins
+  int* cursor;        // [kAllKeys]
   int* counters;      // [kNumCtr]
   int* fb_list;       // [B]
   int* long_list;     // [B]
   float* scratch_main;  // [warps_main][2][kScratchCols] float
   long long* scratch_fb;  // [warps_fb][2][kScratchCols] int64
+  PairDesc* seg_sorted;   // [B] pairs of the segmented kernel, by (shape, period) descending
+  void* seg_items;        // [seg_max_items(B)] SegItem
+  int* seg_item_off;      // [kSegBinsP]
   size_t bytes;
 };
 
 // long_ok: < 0 = DTW (only pairs too long for the bands go to the long-pair list),
 // 0 = no long-pair path (such pairs get NaN / INT64_MIN),
 // else the medium-row threshold (medium_rows_for(B, SMs)) of Fréchet
+// seg: route the Fréchet pairs the segmented kernel takes (seg_bin ≥ 0) to its
+// list and item table (general path only: B > kPrepSmallMax)
 cudaError_t launch_prep(const int64_t* offsets, const int32_t* lengths, int64_t B, int int_out,
                         int long_ok, void* out, const BatchWs& ws, int num_sms, cudaStream_t st,
-                        int64_t* launches);
+                        int64_t* launches, bool seg = false);
 
 }  // namespace ffd

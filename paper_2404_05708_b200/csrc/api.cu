@@ -115,8 +115,8 @@ static BatchWs batch_layout(void* base, int64_t B, int sms) {
   w.scratch_main = reinterpret_cast<float*>(take(warps_main * 2 * kScratchCols * sizeof(float)));
   w.scratch_fb = reinterpret_cast<long long*>(take(warps_fb * 2 * kScratchCols * sizeof(long long)));
   w.seg_sorted = reinterpret_cast<PairDesc*>(take(sizeof(PairDesc) * (size_t)B));
-  w.seg_items = take(sizeof(SegItem) * (size_t)seg_max_items(B));
-  w.seg_item_off = reinterpret_cast<int*>(take(sizeof(int) * kSegBins));
+  w.seg_groups = take(sizeof(SegGroup) * (size_t)seg_max_groups(B));
+  w.seg_off = reinterpret_cast<int*>(take(sizeof(int) * (2 * kSegBins + 3 * kSegShapes)));
   w.bytes = off;
   return w;
 }
@@ -217,15 +217,14 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
       SegProblem sp{};
       sp.p = p;
       sp.q = q;
-      sp.sorted = ws.seg_sorted;
-      sp.items = reinterpret_cast<const SegItem*>(ws.seg_items);
-      sp.n_items = ws.counters + kCtrSegItems;
-      sp.counter = ws.counters + kCtrSegChunk;
+      sp.groups = reinterpret_cast<const SegGroup*>(ws.seg_groups);
+      sp.n_groups = ws.counters + kCtrSegItems;
+      sp.shape_info = ws.seg_off + 2 * kSegBins;
+      sp.shape_ctr = ws.counters + kCtrSegShape;
       sp.out = out;
       sp.fb_list = ws.fb_list;
       sp.fb_count = ws.counters + kCtrFb;
-      if (launch_seg(sp, kind, dim, int_in, fin, di.sms, st) != cudaSuccess) return FFD_ERR_CUDA;
-      ++g_launches;
+      if (launch_seg(sp, kind, dim, int_in, fin, di.sms, st, &g_launches) != cudaSuccess) return FFD_ERR_CUDA;
     }
   }
 

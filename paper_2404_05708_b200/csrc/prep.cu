@@ -25,7 +25,7 @@ __device__ __forceinline__ int pair_key(const int64_t* __restrict__ offsets,
                                         const int32_t* __restrict__ lengths, int64_t B, int64_t k,
                                         int int_out, int long_ok, void* __restrict__ out, PairDesc& d,
                                         int* __restrict__ long_list, int* __restrict__ long_count,
-                                        bool seg = false) {
+                                        int seg = 0) {
   const int n = lengths[k], m = lengths[B + k];
   if (n < 1 || m < 1) {
     write_invalid(out, k, int_out);
@@ -33,7 +33,7 @@ __device__ __forceinline__ int pair_key(const int64_t* __restrict__ offsets,
   }
   if (seg && long_ok > 0) {
     // the segmented kernel (seg.cuh): single-band Fréchet pairs, the longer curve on the rows
-    const int bin = seg_bin(n, m);
+    const int bin = seg_bin(n, m, seg == 2);
     if (bin >= 0) {
       int W, R;
       seg_shape(bin / kSegHB, W, R);
@@ -107,7 +107,7 @@ __global__ void prep_keys_kernel(const int64_t* __restrict__ offsets,
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < B;
        k += (int64_t)gridDim.x * blockDim.x) {
     PairDesc d;
-    const int key = pair_key(offsets, lengths, B, k, int_out, long_ok, out, d, long_list, long_count, seg != 0);
+    const int key = pair_key(offsets, lengths, B, k, int_out, long_ok, out, d, long_list, long_count, seg);
     if (key >= 0) {
       tmp[k] = d;
       atomicAdd(&h[key], 1);
@@ -259,11 +259,11 @@ __device__ int block_scan_excl(int* a, int n) {
 
 // one block of 1024 threads: the batch kernel's bins (descending) as
 // prep_scan_kernel, then the segmented kernel's bins (descending: the largest
-// shape and period first) -> pair cursors, and its items (G·L pairs of one bin
-// each) -> first item per bin (in rank order) and the item count
+// shape and period first) -> pair cursors (and a copy: the bin starts), and its
+// groups (G pairs of one bin each) -> first group per bin (in rank order) and
+// the group count.  off: [kSegBins] first group per rank, [kSegBins] bin starts
 __global__ void __launch_bounds__(1024) prep_scan_seg_kernel(const int* __restrict__ hist, int* __restrict__ cursor,
-                                                             int* __restrict__ item_off, int* __restrict__ counters,
-                                                             int L) {
+                                                             int* __restrict__ off, int* __restrict__ counters) {
   __shared__ int s[kSegBins];
   for (int r = threadIdx.x; r < kNumKeys; r += blockDim.x) s[r] = hist[kNumKeys - 1 - r];
   const int total = block_scan_excl(s, kNumKeys);
@@ -271,41 +271,67 @@ __global__ void __launch_bounds__(1024) prep_scan_seg_kernel(const int* __restri
   __syncthreads();
   for (int r = threadIdx.x; r < kSegBins; r += blockDim.x) s[r] = hist[kNumKeys + kSegBins - 1 - r];
   block_scan_excl(s, kSegBins);
-  for (int r = threadIdx.x; r < kSegBins; r += blockDim.x) cursor[kNumKeys + kSegBins - 1 - r] = s[r];
+  for (int r = threadIdx.x; r < kSegBins; r += blockDim.x) {
+    cursor[kNumKeys + kSegBins - 1 - r] = s[r];
+    off[kSegBins + kSegBins - 1 - r] = s[r];
+  }
   __syncthreads();
   for (int r = threadIdx.x; r < kSegBins; r += blockDim.x) {
-    const int bin = kSegBins - 1 - r, cnt = hist[kNumKeys + bin], gl = seg_item_pairs(bin, L);
-    s[r] = (cnt + gl - 1) / gl;
+    const int bin = kSegBins - 1 - r, cnt = hist[kNumKeys + bin], gp = seg_group_pairs(bin);
+    s[r] = (cnt + gp - 1) / gp;
   }
-  const int items = block_scan_excl(s, kSegBins);
-  for (int r = threadIdx.x; r < kSegBins; r += blockDim.x) item_off[r] = s[r];
+  const int groups = block_scan_excl(s, kSegBins);
+  for (int r = threadIdx.x; r < kSegBins; r += blockDim.x) off[r] = s[r];
+  __syncthreads();
+  // per shape: its groups are contiguous (bins are shape-major): [first, end), and
+  // its work Σ pairs · (W·R rows) · H (the kernel spreads the SMs over the shapes by it)
+  if (threadIdx.x < kSegShapes) {
+    const int sh = threadIdx.x;
+    int W, R;
+    seg_shape(sh, W, R);
+    const int r_lo = kSegBins - 1 - (sh * kSegHB + kSegHB - 1);  // rank of the shape's highest bin
+    int ng = 0;
+    float work = 0.f;
+    for (int b = 0; b < kSegHB; b++) {
+      const int bin = sh * kSegHB + b, cnt = hist[kNumKeys + bin];
+      ng += (cnt + kWarp / W - 1) / (kWarp / W);
+      work += (float)cnt * (float)(W * R) * (float)((b + 1) * kSegHStep);
+    }
+    off[2 * kSegBins + 3 * sh] = off[r_lo];
+    off[2 * kSegBins + 3 * sh + 1] = off[r_lo] + ng;
+    off[2 * kSegBins + 3 * sh + 2] = __float_as_int(work);
+  }
   if (threadIdx.x == 0) {
     counters[kCtrNumSorted] = total;
-    counters[kCtrSegItems] = items;
+    counters[kCtrSegItems] = groups;
   }
 }
 
-// item i -> (first pair, pairs, shape): the bin whose item range holds i
-__global__ void prep_seg_items_kernel(const int* __restrict__ hist, const int* __restrict__ cursor,
-                                      const int* __restrict__ item_off, const int* __restrict__ counters,
-                                      SegItem* __restrict__ items, int64_t max_items, int L) {
+// group i (after the scatter) -> its pair descriptors and shape: the bin whose
+// group range holds i
+__global__ void prep_seg_groups_kernel(const int* __restrict__ hist, const int* __restrict__ off,
+                                       const int* __restrict__ counters, const PairDesc* __restrict__ seg_sorted,
+                                       SegGroup* __restrict__ groups, int64_t max_groups) {
   const int n = counters[kCtrSegItems];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n && i < max_items;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n && i < max_groups;
        i += (int64_t)gridDim.x * blockDim.x) {
-    int lo = 0, hi = kSegBins;  // first rank with item_off > i
+    int lo = 0, hi = kSegBins;  // first rank with a first group > i
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if (item_off[mid] <= i) lo = mid + 1;
+      if (off[mid] <= i) lo = mid + 1;
       else hi = mid;
     }
     const int r = lo - 1, bin = kSegBins - 1 - r;
-    const int gl = seg_item_pairs(bin, L), local = (int)i - item_off[r];
+    const int gp = seg_group_pairs(bin), local = (int)i - off[r];
     const int cnt = hist[kNumKeys + bin];
-    SegItem it;
-    it.start = cursor[kNumKeys + bin] + local * gl;
-    it.count = (int16_t)min(gl, cnt - local * gl);
-    it.shape = (int16_t)(bin / kSegHB);
-    items[i] = it;
+    const int start = off[kSegBins + bin] + local * gp;
+    SegGroup g;
+    g.count = min(gp, cnt - local * gp);
+    g.shape = bin / kSegHB;
+    g.pad[0] = g.pad[1] = 0;
+    g.d[0] = seg_sorted[start];
+    g.d[1] = g.count > 1 ? seg_sorted[start + 1] : g.d[0];
+    groups[i] = g;
   }
 }
 
@@ -328,21 +354,18 @@ cudaError_t launch_prep(const int64_t* offsets, const int32_t* lengths, int64_t 
   if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
   prep_keys_kernel<<<(int)blocks, threads, 0, st>>>(offsets, lengths, B, int_out, long_ok, out, ws.tmp,
                                                     ws.keys, ws.hist, ws.long_list,
-                                                    ws.counters + kCtrLong, seg ? 1 : 0);
+                                                    ws.counters + kCtrLong, seg ? (seg_big() ? 2 : 1) : 0);
+  if (seg) prep_scan_seg_kernel<<<1, 1024, 0, st>>>(ws.hist, ws.cursor, ws.seg_off, ws.counters);
+  else prep_scan_kernel<<<1, kNumKeys, 0, st>>>(ws.hist, ws.cursor, ws.counters + kCtrNumSorted);
+  prep_scatter_kernel<<<(int)blocks, threads, 0, st>>>(ws.tmp, ws.keys, B, ws.cursor, ws.sorted, ws.seg_sorted);
+  *launches += 3;
   if (seg) {
-    const int L = seg_items_per_segment();
-    prep_scan_seg_kernel<<<1, 1024, 0, st>>>(ws.hist, ws.cursor, ws.seg_item_off, ws.counters, L);
-    const int64_t mi = seg_max_items(B);
-    const int ib = (int)((mi + 255) / 256 < (int64_t)num_sms * 4 ? (mi + 255) / 256 : (int64_t)num_sms * 4);
-    prep_seg_items_kernel<<<ib, 256, 0, st>>>(ws.hist, ws.cursor, ws.seg_item_off, ws.counters,
-                                              reinterpret_cast<SegItem*>(ws.seg_items), mi, L);
-    *launches += 2;
-  } else {
-    prep_scan_kernel<<<1, kNumKeys, 0, st>>>(ws.hist, ws.cursor, ws.counters + kCtrNumSorted);
+    const int64_t mg = seg_max_groups(B);
+    const int gb = (int)((mg + 255) / 256 < (int64_t)num_sms * 4 ? (mg + 255) / 256 : (int64_t)num_sms * 4);
+    prep_seg_groups_kernel<<<gb, 256, 0, st>>>(ws.hist, ws.seg_off, ws.counters, ws.seg_sorted,
+                                               reinterpret_cast<SegGroup*>(ws.seg_groups), mg);
     *launches += 1;
   }
-  prep_scatter_kernel<<<(int)blocks, threads, 0, st>>>(ws.tmp, ws.keys, B, ws.cursor, ws.sorted, ws.seg_sorted);
-  *launches += 2;
   return cudaGetLastError();
 }
 

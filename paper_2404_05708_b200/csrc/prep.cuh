@@ -9,7 +9,7 @@
 namespace ffd {
 
 constexpr int kNumKeys = kMaxBands * kMaxR;  // 256 shape bins of the batch kernel
-constexpr int kSegBinsP = 16 * 65;          // (shape, period) bins of the segmented kernel (seg.cuh kSegBins)
+constexpr int kSegBinsP = 24 * 65;          // (shape, period) bins of the segmented kernel (seg.cuh kSegBins)
 constexpr int kAllKeys = kNumKeys + kSegBinsP;
 constexpr int64_t kPrepSmallMax = 4096;      // batches up to this size: one-block prep
 
@@ -49,9 +49,10 @@ enum : int {
   kCtrFb = 3,
   kCtrLong = 4,
   kCtrChunkLong = 5,
-  kCtrSegItems = 6,  // items of the segmented kernel
-  kCtrSegChunk = 7,  // its item pop counter
-  kNumCtr = 8
+  kCtrSegItems = 6,  // groups of the segmented kernel
+  kCtrSegChunk = 7,  // (unused: the segmented kernel pops per shape)
+  kCtrSegShape = 8,  // [2] group pop counters of the segmented kernels (small, big)
+  kNumCtr = 32
 };
 
 struct BatchWs {
@@ -66,8 +67,9 @@ struct BatchWs {
   float* scratch_main;  // [warps_main][2][kScratchCols] float
   long long* scratch_fb;  // [warps_fb][2][kScratchCols] int64
   PairDesc* seg_sorted;   // [B] pairs of the segmented kernel, by (shape, period) descending
-  void* seg_items;        // [seg_max_items(B)] SegItem
-  int* seg_item_off;      // [kSegBinsP]
+  void* seg_groups;       // [seg_max_groups(B)] SegGroup
+  int* seg_off;           // [2 · kSegBinsP + 3 · 24]: first group per bin rank, bin starts, per shape
+                          // (first group, end, work as float bits)
   size_t bytes;
 };
 

@@ -6,37 +6,21 @@
 
 namespace ffd {
 
-namespace {
-template <int KIND, int D, bool INT_IN, int FIN>
-cudaError_t launch_k(const SegProblem& pb, int sms, cudaStream_t st) {
-  auto k = seg_kernel<KIND, D, INT_IN, FIN>;
-  const size_t smem = sizeof(SegSmem<KIND, D, INT_IN>) * kWarpsPerCta;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  static int occ_cache[64] = {0};
-  int occ = dev < 64 ? occ_cache[dev] : 0;
-  if (occ == 0) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kWarp * kWarpsPerCta, smem);
-    if (occ < 1) occ = 1;
-    if (dev < 64) occ_cache[dev] = occ;
-  }
-  k<<<sms * occ, kWarp * kWarpsPerCta, smem, st>>>(pb);
-  return cudaGetLastError();
+// one translation unit per built cell (seg_<cell>.cu, compiled in parallel)
+cudaError_t launch_seg_xsq_d2(const SegProblem& pb, int sms, cudaStream_t st, bool big);
+cudaError_t launch_seg_sq_d2_sqrt(const SegProblem& pb, int sms, cudaStream_t st, bool big);
+cudaError_t launch_seg_sq_d2(const SegProblem& pb, int sms, cudaStream_t st, bool big);
+
+// rows above 256 on two 16-lane segments of up to 32 rows per lane (the big
+// kernel, 234 registers: 8 warps/SM).  Measured on config 2: 13 % fewer
+// instructions but 51 % issue, 2.69 against 2.65 ms — off unless FFD_SEG_BIG=1
+bool seg_big() {
+  static const bool on = getenv("FFD_SEG_BIG") && atoi(getenv("FFD_SEG_BIG")) == 1;
+  return on;
 }
-}  // namespace
 
 // built: the exact-integer 2-D squared-L2 cell (config 2) and the fp32 2-D L2 /
 // squared-L2 cells; every other kind stays on the batch kernel
-int seg_items_per_segment() {
-  static const int L = [] {
-    const char* e = getenv("FFD_SEG_L");
-    const int v = e ? atoi(e) : kSegL;
-    return v < 2 ? 2 : (v > kSegMaxL ? kSegMaxL : v);
-  }();
-  return L;
-}
-
 bool seg_supported(int kind, int dim, int int_in, int fin) {
   static const int off = getenv("FFD_SEG") && atoi(getenv("FFD_SEG")) == 0;
   if (off || dim != 2) return false;
@@ -44,10 +28,13 @@ bool seg_supported(int kind, int dim, int int_in, int fin) {
   return kind == K_SQ && (fin == F_SQRT || fin == F_NONE);
 }
 
-cudaError_t launch_seg(const SegProblem& pb, int kind, int dim, int int_in, int fin, int sms, cudaStream_t st) {
-  if (dim == 2 && int_in && kind == K_XSQ) return launch_k<K_XSQ, 2, true, F_NONE>(pb, sms, st);
-  if (dim == 2 && !int_in && kind == K_SQ && fin == F_SQRT) return launch_k<K_SQ, 2, false, F_SQRT>(pb, sms, st);
-  if (dim == 2 && !int_in && kind == K_SQ && fin == F_NONE) return launch_k<K_SQ, 2, false, F_NONE>(pb, sms, st);
+cudaError_t launch_seg(const SegProblem& pb, int kind, int dim, int int_in, int fin, int sms, cudaStream_t st,
+                       int64_t* launches) {
+  const bool big = seg_big();
+  *launches += big ? 2 : 1;
+  if (dim == 2 && int_in && kind == K_XSQ) return launch_seg_xsq_d2(pb, sms, st, big);
+  if (dim == 2 && !int_in && kind == K_SQ && fin == F_SQRT) return launch_seg_sq_d2_sqrt(pb, sms, st, big);
+  if (dim == 2 && !int_in && kind == K_SQ && fin == F_NONE) return launch_seg_sq_d2(pb, sms, st, big);
   return cudaErrorInvalidValue;
 }
 

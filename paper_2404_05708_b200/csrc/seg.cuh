@@ -1,5 +1,5 @@
 // seg.cuh — segmented two-column kernel for batches of single-band pairs
-// (SURVEY §8(a) a1–a6; BASELINE configs 2 and 1-like shapes).
+// (SURVEY §8(a) a1–a6; BASELINE config 2 and every 2-D pair ≤ 512 points).
 //
 // What: δ_dF of every pair, Eq. (1) M_ij = max{min{M_{i-1,j}, M_{i-1,j-1},
 // M_{i,j-1}}, d_ij}, linear state (Theorem 1; Alg. 5,
@@ -13,143 +13,216 @@
 //     processes stream positions 2(t−s), 2(t−s)+1 at warp step t: two columns
 //     per step, the second column's chain trailing the first by one row, so the
 //     shuffle + min/max chain latency is paid once per two columns.
-//   * A work ITEM is G·L pairs of the same (W, R) and nearly the same column
-//     count; every pair's stream is padded to the item's period 2H (sentinel +
-//     columns + repeats of its last column: exact for δ_dF), segment h runs
-//     pairs h, h+G, h+2G, … back to back.  All segments therefore switch pairs
-//     at the same steps: the result of pair k leaves at step H(k+1)+W−1, the
-//     corner value enters at step Hk, and lane s takes pair k's rows at step
-//     Hk+s — one predicated shared-memory load per row vector in a W-step
-//     window, no divergent per-lane events.
-//   * Row strips of the next pair are staged in shared memory (cp.async, then
-//     converted: int input is translated by the pair's first row point into
-//     the fp32-exact window) during the current pair.
+//   * A GROUP is G pairs of the same (W, R) and nearly the same column count
+//     (the prep sorts pairs by (shape, period)); its streams are padded to the
+//     group's period 2H (sentinel + columns + repeats of the last column: exact
+//     for δ_dF), one pair per segment.  A warp runs a STREAM of groups of one
+//     shape back to back: group k occupies steps [T_k, T_k + H_k) of lane 0, so
+//     every segment switches pairs at the same steps — the corner value enters
+//     at T_k, lane s takes group k's rows at T_k + s (one predicated shared
+//     load per 4 rows in a W-step window), and group k − 1's result is complete
+//     in the segment's last lane before T_k + W − 1.  Only a change of shape
+//     (or the end of the list) drains the lane pipeline (W − 1 steps).
+//   * Groups are popped one ahead (atomic counter; the group record holds its
+//     pair descriptors, so one dependent load), accepted at the first ring
+//     refill of the previous group, and their rows staged in shared memory
+//     (cp.async, then converted: int input is translated by the pair's first row
+//     point into the fp32-exact window) after its window.
 //   * Column points are fetched one 32-position chunk ahead into registers and
 //     written into a per-warp ring (one LDS.128 per column per lane).
-//   * Items come from a list sorted by (shape, period), largest first (PAPER
-//     L261–L262), popped by persistent warps.
+//   * Groups come from a list sorted by (shape, period), largest first (PAPER
+//     L261–L262): all warps move through it together, so an SM runs few shapes
+//     at a time (their code shares the instruction cache).
 #pragma once
 #include "prep.cuh"
 #include "strip.cuh"
 
 namespace ffd {
 
-constexpr int kSegL = 2;           // pairs per segment per item (default; FFD_SEG_L = 2 … 8 at run time:
-                                   // larger items put more shapes in flight at once and thrash the
-                                   // instruction cache — L = 8 measured 3.7 against 2.6 ms on config 2)
-constexpr int kSegMaxL = 8;
-constexpr int kSegMaxItemPairs = 2 * kSegMaxL;  // G·L ≤ 16
-constexpr int kSegRows = 512;      // rows per warp: G·W·R ≤ 512
+constexpr int kSegRows = 512;      // longest rows curve of a segmented pair
+constexpr int kSegRowsBig = 1024;  // stage rows of the big kernel (2 segments × 16 lanes × R ≤ 32)
 constexpr int kSegHStep = 4;       // period buckets of 4 steps
 constexpr int kSegHB = 65;         // H ≤ 257 (columns ≤ 512)
-constexpr int kSegShapes = 16;     // W = 16: R ∈ {2, 4, …, 16};  W = 32: R ∈ {9, …, 16}
+constexpr int kSegShapes = 24;     // 0–7: W = 16, R ∈ {2, 4, …, 16};  8–15: W = 32, R ∈ {9, …, 16};
+                                   // 16–23 (the big kernel): W = 16, R ∈ {18, 20, …, 32}
+constexpr int kSegSmallShapes = 16;
 constexpr int kSegBins = kSegShapes * kSegHB;
-constexpr int kSegLag = 32;        // H ≥ W + kSegLag: a pair's row staging finishes in its predecessor
+constexpr int kSegLag = 32;        // H ≥ W + kSegLag: a group's rows are staged inside its predecessor
+constexpr int kSegSlots = 4;       // group records per warp (current, next, two finished)
 static_assert(kSegBins == kSegBinsP, "prep.cuh bin count");
 
 __host__ __device__ inline void seg_shape(int idx, int& W, int& R) {
   if (idx < 8) {
     W = 16;
     R = 2 * (idx + 1);
-  } else {
+  } else if (idx < 16) {
     W = 32;
     R = idx + 1;
+  } else {
+    W = 16;
+    R = 2 * (idx - 7);
   }
 }
-// (W, R) shape for a rows curve of `rows` ≤ 512 points: rows padded to a multiple of 32
-__host__ __device__ inline int seg_shape_for(int rows) {
-  if (rows <= 256) {
+// (W, R) shape for a rows curve of `rows` ≤ 512 points: rows padded to a multiple
+// of 32.  big: rows above 256 take two 16-lane segments of up to 32 rows per lane
+// (the big kernel) instead of one 32-lane segment of up to 16
+__host__ __device__ inline int seg_shape_for(int rows, bool big) {
+  if (rows <= 256 || big) {
     int R = (rows + 15) / 16;
     R += R & 1;
-    return R / 2 - 1;
+    return R <= 16 ? R / 2 - 1 : R / 2 + 7;
   }
   return (rows + 31) / 32 - 1;
 }
 __host__ __device__ inline int seg_period(int cols) { return (cols + 2) / 2; }  // H: 2H ≥ 1 + cols
 // seg key of a Fréchet pair (n, m), or −1 if it stays on the batch kernel
-__host__ __device__ inline int seg_bin(int n, int m) {
+__host__ __device__ inline int seg_bin(int n, int m, bool big) {
   const int rows = n > m ? n : m, cols = n > m ? m : n;
   if (rows > kSegRows) return -1;
   int W, R;
-  const int sh = seg_shape_for(rows);
+  const int sh = seg_shape_for(rows, big);
   seg_shape(sh, W, R);
   const int H = seg_period(cols);
   if (H < W + kSegLag) return -1;
   return sh * kSegHB + (H - 1) / kSegHStep;
 }
-__host__ __device__ inline int seg_item_pairs(int bin, int L) {
+__host__ __device__ inline int seg_group_pairs(int bin) {
   int W, R;
   seg_shape(bin / kSegHB, W, R);
-  return (kWarp / W) * L;
+  return kWarp / W;
 }
 
-struct SegItem {
-  int start;      // first pair in the seg-sorted list
-  int16_t count;  // pairs (≤ G·L)
-  int16_t shape;  // (W, R) index
+// one group: G ≤ 2 pair descriptors (rows = the longer curve) and its shape
+struct alignas(16) SegGroup {
+  PairDesc d[2];
+  int count;  // pairs (1 … G)
+  int shape;  // (W, R) index
+  int pad[2];
 };
+static_assert(sizeof(SegGroup) == 80, "SegGroup");
 
 struct SegProblem {
   const void* p;
   const void* q;
-  const PairDesc* sorted;  // seg-sorted pairs (rows = the longer curve)
-  const SegItem* items;
-  const int* n_items;
-  int* counter;
+  const SegGroup* groups;
+  const int* n_groups;
+  const int* shape_info;  // [16][3]: first group, end, work (float bits) of each shape
+  int* shape_ctr;         // [2] groups popped by the small and the big kernel
   void* out;
   int* fb_list;  // int input: pairs that left the fp32-exact window (exact int64 tier)
   int* fb_count;
 };
 
-template <int KIND, int D, bool INT_IN>
-struct alignas(16) SegSmem {
-  using C = SCfg<float, KIND, D, INT_IN>;
-  uint4 ring[128 * C::EW];               // 128 positions (G = 1) or 2 × 64 (G = 2)
-  float stage[C::NS][kSegRows];          // next pair's row strips, [c][h·W·RP + s·RP + r]
-  int32_t raw[INT_IN ? kSegRows * D : 4];  // int input: raw points (cp.async target)
-  const void* rows_ptr[kSegMaxItemPairs];
-  const void* cols_ptr[kSegMaxItemPairs];
-  int nrows[kSegMaxItemPairs];
-  int ncols[kSegMaxItemPairs];
-  int idx[kSegMaxItemPairs];
-  int bad[kSegMaxItemPairs];
-  int center[kSegMaxItemPairs][D];
+// a popped group, held in registers until it is accepted into a stream
+struct SegLook {
+  PairDesc d;  // lanes < G: pair `lane` of the group
+  int count;   // 0: no group (the list is exhausted)
+  int shape;
 };
 
-template <int KIND, int D, bool INT_IN, int FIN, int W, int R>
+template <int D>
+struct SegSlot {
+  const void* rows_ptr[2];
+  const void* cols_ptr[2];
+  int nrows[2];
+  int ncols[2];
+  int idx[2];
+  int bad[2];
+  int center[2][D];
+  int count;
+};
+
+template <int KIND, int D, bool INT_IN, int ROWS>
+struct alignas(16) SegSmem {
+  using C = SCfg<float, KIND, D, INT_IN>;
+  uint4 ring[128 * C::EW];  // 128 positions (G = 1) or 2 × 64 (G = 2)
+  float stage[C::NS][ROWS]; // the next group's row strips, [c][h·W·RP + s·RP + r] (int input:
+                            // copied as int32 bits, converted in place)
+  SegSlot<D> slot[kSegSlots];
+};
+
+// Pop the next group of this kernel's shapes [LO, LO + NSH): the list holds them
+// contiguously (descending shape index), from the first group of the highest
+// shape to the end of the lowest; one atomic counter per kernel (lane 0), the
+// record's loads are left in flight.  All warps move through the list together,
+// so an SM runs few shapes at a time (measured: spreading the SMs over the
+// shapes by their work lost 2.49 -> 2.65 ms on config 2).
+template <int LO, int NSH>
+__device__ __forceinline__ void seg_pop(const SegProblem& pb, int lane, SegLook& L) {
+  int g = 0, end = 0;
+  if (lane == 0) {
+    const int first = pb.shape_info[3 * (LO + NSH - 1)];
+    end = pb.shape_info[3 * LO + 1];
+    g = first + atomicAdd(pb.shape_ctr + (LO > 0 ? 1 : 0), 1);
+  }
+  g = __shfl_sync(0xffffffffu, g, 0);
+  end = __shfl_sync(0xffffffffu, end, 0);
+  L.count = 0;
+  L.shape = -1;
+  if (g < end) {
+    const SegGroup* gp = pb.groups + g;
+    L.d = gp->d[lane & 1];
+    L.count = gp->count;
+    L.shape = gp->shape;
+  }
+}
+
+template <int KIND, int D, bool INT_IN, int FIN, int W, int R, int ROWS, int LO, int NSH>
 struct SegRunner {
   using C = SCfg<float, KIND, D, INT_IN>;
   using In = typename std::conditional<INT_IN, int32_t, float>::type;
-  using Sm = SegSmem<KIND, D, INT_IN>;
+  using Sm = SegSmem<KIND, D, INT_IN, ROWS>;
   static constexpr int G = kWarp / W;     // segments per warp
   static constexpr int RING = 128 / G;    // ring positions per segment
   static constexpr int RP = (R + 3) & ~3; // lane stride in the stage arrays (16-B aligned)
   static constexpr int NS = C::NS;
   static constexpr int EW = C::EW;
-  static_assert(G * W * RP <= kSegRows, "stage arrays");
-  static_assert(!INT_IN || G * W * R <= kSegRows, "raw stage");
+  static constexpr int SHAPE = W == 32 ? R - 1 : (R <= 16 ? R / 2 - 1 : R / 2 + 7);
+  static_assert(G * W * RP <= ROWS, "stage arrays");
 
   Sm& sm;
   const SegProblem& pb;
   const int lane, s, h;
-  int count, H, Lh;
 
-  __device__ SegRunner(Sm& m, const SegProblem& p, int l)
-      : sm(m), pb(p), lane(l), s(l % W), h(l / W) {}
+  __device__ SegRunner(Sm& m, const SegProblem& p, int l) : sm(m), pb(p), lane(l), s(l % W), h(l / W) {}
 
-  // pair slot of segment hh in sequence position k (a missing pair reads pair 0)
-  __device__ __forceinline__ int slot(int hh, int k) const {
-    const int j = hh + G * k;
-    return j < count ? j : 0;
+  // the group record L into slot j
+  __device__ __forceinline__ void accept(const SegLook& L, int j) {
+    SegSlot<D>& S = sm.slot[j];
+    if (lane < L.count) {
+      const PairDesc& d = L.d;
+      const In* rp = reinterpret_cast<const In*>(d.swap ? pb.q : pb.p) + d.row_off * D;
+      const In* cp = reinterpret_cast<const In*>(d.swap ? pb.p : pb.q) + d.col_off * D;
+      S.rows_ptr[lane] = rp;
+      S.cols_ptr[lane] = cp;
+      S.nrows[lane] = d.n_rows;
+      S.ncols[lane] = d.m_cols;
+      S.idx[lane] = d.idx;
+      S.bad[lane] = 0;
+      if constexpr (INT_IN) {
+#pragma unroll
+        for (int c = 0; c < D; c++) S.center[lane][c] = (int)rp[c];
+      }
+    }
+    if (lane == 0) S.count = L.count;
+    __syncwarp();
+  }
+  // period of the group in slot j (uniform)
+  __device__ __forceinline__ int period(int j) const {
+    const int m = lane < sm.slot[j].count ? sm.slot[j].ncols[lane] : 0;
+    return seg_period(__reduce_max_sync(0xffffffffu, m));
   }
 
-  // one input point of pair j translated into the fp32-exact window (int input)
-  __device__ __forceinline__ bool conv(const In (&a)[D], int j, float (&v)[D]) const {
+  // pair of segment hh in slot j (a segment without a pair reads pair 0)
+  __device__ __forceinline__ int pair_of(int j, int hh) const { return hh < sm.slot[j].count ? hh : 0; }
+
+  // one input point of pair (j, pr) translated into the fp32-exact window (int input)
+  __device__ __forceinline__ bool conv(const In (&a)[D], int j, int pr, float (&v)[D]) const {
     bool ok = true;
 #pragma unroll
     for (int c = 0; c < D; c++) {
       if constexpr (INT_IN) {
-        const long long t = (long long)a[c] - (long long)sm.center[j][c];
+        const long long t = (long long)a[c] - (long long)sm.slot[j].center[pr][c];
         ok &= (t >= -C::LIM) && (t <= C::LIM);
         v[c] = (float)(int)t;
       } else {
@@ -159,40 +232,34 @@ struct SegRunner {
     return ok;
   }
 
-  // ---- row strips: stage pair k of every segment (cp.async), then convert ----
-  __device__ __forceinline__ void stage_issue(int k) {
+  // ---- row strips: stage the group in slot j (cp.async), then convert --------
+  __device__ __forceinline__ void stage_issue(int j) {
     for (int i = lane; i < G * W * R; i += kWarp) {
       const int hh = i / (W * R), rr = i - hh * (W * R);
-      const int j = slot(hh, k);
-      const int row = min(rr, sm.nrows[j] - 1);
-      const In* src = reinterpret_cast<const In*>(sm.rows_ptr[j]) + (int64_t)row * D;
+      const int pr = pair_of(j, hh);
+      const int row = min(rr, sm.slot[j].nrows[pr] - 1);
+      const In* src = reinterpret_cast<const In*>(sm.slot[j].rows_ptr[pr]) + (int64_t)row * D;
 #pragma unroll
       for (int c = 0; c < D; c++) {
-        uint32_t dst;
-        if constexpr (INT_IN) dst = (uint32_t)__cvta_generic_to_shared(&sm.raw[i * D + c]);
-        else dst = (uint32_t)__cvta_generic_to_shared(&sm.stage[c][hh * W * RP + (rr / R) * RP + rr % R]);
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&sm.stage[c][hh * W * RP + (rr / R) * RP + rr % R]);
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src + c) : "memory");
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  __device__ __forceinline__ void stage_finish(int k) {
+  __device__ __forceinline__ void stage_finish(int j) {
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncwarp();
-    if constexpr (INT_IN || C::XSQ) {
+    if constexpr (INT_IN) {
       for (int i = lane; i < G * W * R; i += kWarp) {
         const int hh = i / (W * R), rr = i - hh * (W * R);
-        const int j = slot(hh, k);
+        const int pr = pair_of(j, hh);
+        const int o = hh * W * RP + (rr / R) * RP + rr % R;
         In a[D];
         float v[D];
 #pragma unroll
-        for (int c = 0; c < D; c++) {
-          if constexpr (INT_IN) a[c] = sm.raw[i * D + c];
-          else a[c] = sm.stage[c][hh * W * RP + (rr / R) * RP + rr % R];
-        }
-        const bool ok = conv(a, j, v);
-        if (!ok) sm.bad[j] = 1;
-        const int o = hh * W * RP + (rr / R) * RP + rr % R;
+        for (int c = 0; c < D; c++) a[c] = __float_as_int(sm.stage[c][o]);
+        if (!conv(a, j, pr, v)) sm.slot[j].bad[pr] = 1;
 #pragma unroll
         for (int c = 0; c < D; c++) sm.stage[c][o] = v[c];
         if constexpr (C::XSQ) {
@@ -209,27 +276,32 @@ struct SegRunner {
   // load per 4 rows); sa: shared address of this lane's strip of coordinate 0
   __device__ __forceinline__ void take_rows(float (&x)[NS][R], uint32_t sa, int p) const {
 #pragma unroll
-    for (int c = 0; c < NS; c++) pred_lds_strip<R>(x[c], sa + c * kSegRows * 4, p);
+    for (int c = 0; c < NS; c++) pred_lds_strip<R>(x[c], sa + c * ROWS * 4, p);
   }
 
-  // ---- column stream of segment hh: position pos → element ------------------
+  // ---- column stream of this segment: position pos → element ----------------
   struct Raw {
     In a[D];
-    int j;     // pair slot
-    int kind;  // 0 point, 1 sentinel / past the end
+    int j, pr;  // slot, pair
+    int kind;   // 0 point, 1 sentinel
   };
-  __device__ __forceinline__ void fetch(int pos, Raw& r) const {
+  // pos lies in group k (slot jk, from step Tk) or — when the next group is
+  // accepted (Tn ≥ 0) — possibly in it (slot jn, from step Tn).  Positions past
+  // the stream's last group repeat its last column (they only reach the drain).
+  __device__ __forceinline__ void fetch(int pos, int jk, int Tk, int jn, int Tn, Raw& r) const {
 #pragma unroll
     for (int c = 0; c < D; c++) r.a[c] = (In)0;
-    const int k = pos / (2 * H), loc = pos - k * 2 * H;
-    r.j = slot(h, k < Lh ? k : 0);
-    if (k >= Lh || loc == 0) {
+    const bool nxt = Tn >= 0 && pos >= 2 * Tn;
+    r.j = nxt ? jn : jk;
+    r.pr = pair_of(r.j, h);
+    const int loc = pos - 2 * (nxt ? Tn : Tk);
+    if (loc == 0) {
       r.kind = 1;
       return;
     }
     r.kind = 0;
-    const int col = min(loc - 1, sm.ncols[r.j] - 1);
-    const In* src = reinterpret_cast<const In*>(sm.cols_ptr[r.j]) + (int64_t)col * D;
+    const int col = min(loc - 1, sm.slot[r.j].ncols[r.pr] - 1);
+    const In* src = reinterpret_cast<const In*>(sm.slot[r.j].cols_ptr[r.pr]) + (int64_t)col * D;
 #pragma unroll
     for (int c = 0; c < D; c++) r.a[c] = __ldg(src + c);
   }
@@ -251,7 +323,7 @@ struct SegRunner {
       }
     } else {
       float v[D];
-      if (!conv(r.a, r.j, v)) sm.bad[r.j] = 1;
+      if (!conv(r.a, r.j, r.pr, v)) sm.slot[r.j].bad[r.pr] = 1;
       if constexpr (C::XSQ) {
         int qq = 0;
 #pragma unroll
@@ -270,13 +342,12 @@ struct SegRunner {
     for (int w = 0; w < EW; w++) dst[w] = reinterpret_cast<const uint4*>(e)[w];
   }
 
-  // ---- result of the pair in slot (h, k): the segment's last lane ------------
-  __device__ __forceinline__ void emit(int k, float v) {
-    const int j = h + G * k;
-    if (s != W - 1 || j >= count) return;
-    const int idx = sm.idx[j];
+  // ---- result of this segment's pair in slot j: the segment's last lane ------
+  __device__ __forceinline__ void emit(int j, float v) {
+    if (s != W - 1 || h >= sm.slot[j].count) return;
+    const int idx = sm.slot[j].idx[h];
     if constexpr (INT_IN) {
-      if (sm.bad[j]) {
+      if (sm.slot[j].bad[h]) {
         pb.fb_list[atomicAdd(pb.fb_count, 1)] = idx;
         return;
       }
@@ -287,11 +358,15 @@ struct SegRunner {
     }
   }
 
-  __device__ void run() {
-    const int NT = H * Lh;         // steps until lane 0 has consumed every position
-    const int total = NT + W - 1;  // the segment's last lane finishes W − 1 steps later
+  // One stream: `look` holds its first group (of this shape); groups of the same
+  // shape follow until the list ends or a group of another shape is popped —
+  // that one is left in `look` for the caller.
+  __device__ void stream(SegLook& look) {
+    constexpr int SM = kSegSlots - 1;
     float x[NS][R], c[R];
-    // rows of the first pair of every segment
+    accept(look, 0);  // group 0 → slot 0
+    int H = period(0);
+    seg_pop<LO, NSH>(pb, lane, look);  // the next group, in flight
     stage_issue(0);
     stage_finish(0);
 #pragma unroll
@@ -300,17 +375,21 @@ struct SegRunner {
       for (int r = 0; r < R; r++) x[cc][r] = sm.stage[cc][h * W * RP + s * RP + r];
 #pragma unroll
     for (int r = 0; r < R; r++) c[r] = finf();
+    // stream state (uniform): group k in slot k & SM from step Tk with period H;
+    // the next group (once accepted) from step Tn (−1: not decided, or none)
+    int k = 0, Tk = 0, Tn = -1;
+    bool decided = false, last = false;  // next group decided; group k is the stream's last
+    bool staging = false, stage_due = false;
     // column ring: positions [0, 32) of every segment stored, [32, 64) prefetched
     Raw pre[G];
 #pragma unroll
     for (int e = 0; e < G; e++) {
       Raw r0;
-      fetch(s * G + e, r0);
+      fetch(s * G + e, 0, 0, 0, -1, r0);
       store(s * G + e, r0);
-      fetch(32 + s * G + e, pre[e]);
+      fetch(32 + s * G + e, 0, 0, 0, -1, pre[e]);
     }
     __syncwarp();
-    __syncwarp();  // stage arrays read by every lane before the next staging overwrites them
 
     float diag = finf(), b0v = finf();
     // one step on positions 2g, 2g+1 of this segment; top0: what the segment's
@@ -359,41 +438,51 @@ struct SegRunner {
       diag = up1;
     };
     int next_refill = 16;  // 32 positions per segment per refill
-    int stage_k = 1;       // next pair (sequence position) to stage
-    bool staging = false;  // cp.async of stage_k − 1 in flight
-    // every 16 steps: the chunk of positions [2t, 2t+32) is stored, the next one
-    // prefetched; the row staging of the next pair is issued at the first refill
-    // after the current pair's window and finished at the one after that
+    // every 16 steps: positions [2t, 2t+32) stored, the next chunk prefetched.
+    // Group k + 1 is accepted (or the stream's end decided) at the first refill
+    // of group k, its rows staged at the first refill after group k's window and
+    // converted at the next one (H ≥ W + 32: done before group k + 1 starts).
     auto refill = [&](int t) {
+      if (staging) {
+        stage_finish((k + 1) & SM);
+        staging = false;
+      } else if (stage_due && t >= Tk + W) {
+        stage_issue((k + 1) & SM);
+        staging = true;
+        stage_due = false;
+      }
+      if (!decided) {
+        decided = true;
+        if (look.count > 0 && look.shape == SHAPE) {
+          accept(look, (k + 1) & SM);
+          Tn = Tk + H;
+          stage_due = true;
+          seg_pop<LO, NSH>(pb, lane, look);  // the group after it, in flight
+        } else {
+          last = true;
+        }
+      }
 #pragma unroll
       for (int e = 0; e < G; e++) {
         store(2 * t + s * G + e, pre[e]);
-        fetch(2 * t + 32 + s * G + e, pre[e]);
-      }
-      if (staging) {
-        stage_finish(stage_k - 1);
-        staging = false;
-      } else if (stage_k < Lh && t >= H * (stage_k - 1) + W) {
-        stage_issue(stage_k);
-        ++stage_k;
-        staging = true;
+        fetch(2 * t + 32 + s * G + e, k & SM, Tk, (k + 1) & SM, last ? -1 : Tn, pre[e]);
       }
       next_refill += 16;
       __syncwarp();
     };
     const uint32_t stage_sa = (uint32_t)__cvta_generic_to_shared(&sm.stage[0][h * W * RP + s * RP]);
-    float res = finf();  // the segment's last lane: result of the pair before the window
+    float res = finf();  // the segment's last lane: result of the group before the window
     int t = 0;
-    for (int k = 0; k < Lh; k++) {
-      const int t0 = H * k, tw = t0 + W, t1 = t0 + H;
-      // step Hk: the sentinel of pair k reaches lane 0 (corner value 0 above its first row)
+    while (true) {
+      const int t0 = Tk, tw = t0 + W, t1 = t0 + H;
+      // step Tk: the sentinel of group k reaches lane 0 (corner value 0 above its first row)
       if (t == next_refill) refill(t);
       if (k > 0) take_rows(x, stage_sa, s == 0);
       step(t, 0.f);
       ++t;
       if (k > 0) {
-        // the rest of the window: lane s takes pair k's rows at step Hk + s; the
-        // last lane keeps its value of pair k − 1 (complete before its switch)
+        // the rest of the window: lane s takes group k's rows at step Tk + s; the
+        // last lane keeps its value of group k − 1 (complete before its switch)
         while (t < tw) {
           const int stop = min(next_refill, tw);
 #pragma unroll 2
@@ -405,7 +494,7 @@ struct SegRunner {
           }
           if (t == next_refill && t < tw) refill(t);
         }
-        emit(k - 1, res);
+        emit((k - 1) & SM, res);
       }
       while (t < t1) {
         const int stop = min(next_refill, t1);
@@ -413,98 +502,120 @@ struct SegRunner {
         for (; t < stop; ++t) step(t, finf());
         if (t == next_refill && t < t1) refill(t);
       }
+      if (last) break;
+      // the next group: its rows staged, its first positions already in the ring
+      ++k;
+      Tk = Tn;
+      H = period(k & SM);
+      Tn = -1;
+      decided = false;
     }
-    for (; t < total; t++) {  // drain: positions past the stream's end
+    // drain: positions past the stream's end reach the last lanes
+    for (const int total = t + W - 1; t < total; t++) {
       if (t == next_refill) refill(t);
       step(t, finf());
     }
-    emit(Lh - 1, c[R - 1]);
+    emit(k & SM, c[R - 1]);
     __syncwarp();
   }
 };
 
-template <int KIND, int D, bool INT_IN, int FIN>
-__global__ void __launch_bounds__(kWarp* kWarpsPerCta, 4) seg_kernel(const SegProblem pb) {
-  using Sm = SegSmem<KIND, D, INT_IN>;
+// BIG = false: shapes 0–15 (≤ 16 rows per lane, 4 CTAs/SM); BIG = true: shapes
+// 16–23 (18–32 rows per lane, 2 CTAs/SM for their registers)
+template <int KIND, int D, bool INT_IN, int FIN, bool BIG>
+__global__ void __launch_bounds__(kWarp* kWarpsPerCta, BIG ? 2 : 4) seg_kernel(const SegProblem pb) {
+  constexpr int ROWS = BIG ? kSegRowsBig : kSegRows;
+  constexpr int LO = BIG ? kSegSmallShapes : 0, NSH = BIG ? kSegShapes - kSegSmallShapes : kSegSmallShapes;
+  using Sm = SegSmem<KIND, D, INT_IN, ROWS>;
   extern __shared__ uint4 seg_dyn[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   Sm& sm = reinterpret_cast<Sm*>(seg_dyn)[warp];
   for (int i = lane; i < 128 * SCfg<float, KIND, D, INT_IN>::EW; i += kWarp) sm.ring[i] = make_uint4(0u, 0u, 0u, 0u);
   __syncwarp();
-  const int n_items = *pb.n_items;
-  while (true) {
-    int item = 0;
-    if (lane == 0) item = atomicAdd(pb.counter, 1);
-    item = __shfl_sync(0xffffffffu, item, 0);
-    if (item >= n_items) break;
-    const SegItem it = pb.items[item];
-    int m = 0;
-    if (lane < it.count) {
-      const PairDesc d = pb.sorted[it.start + lane];
-      using In = typename std::conditional<INT_IN, int32_t, float>::type;
-      const In* rp = reinterpret_cast<const In*>(d.swap ? pb.q : pb.p) + d.row_off * D;
-      const In* cp = reinterpret_cast<const In*>(d.swap ? pb.p : pb.q) + d.col_off * D;
-      sm.rows_ptr[lane] = rp;
-      sm.cols_ptr[lane] = cp;
-      sm.nrows[lane] = d.n_rows;
-      sm.ncols[lane] = d.m_cols;
-      sm.idx[lane] = d.idx;
-      sm.bad[lane] = 0;
-      if constexpr (INT_IN) {
-#pragma unroll
-        for (int c = 0; c < D; c++) sm.center[lane][c] = (int)rp[c];
-      }
-      m = d.m_cols;
-    }
-    const int H = seg_period(__reduce_max_sync(0xffffffffu, m));
-    __syncwarp();
-    auto go = [&](auto& run) {
-      run.count = it.count;
-      run.H = H;
-      run.Lh = (it.count + run.G - 1) / run.G;
-      run.run();
-    };
-#define FFD_SEG_CASE(IDX, WW, RR)                              \
-  case IDX: {                                                  \
-    SegRunner<KIND, D, INT_IN, FIN, WW, RR> run(sm, pb, lane); \
-    go(run);                                                   \
-    break;                                                     \
+  SegLook look;
+  seg_pop<LO, NSH>(pb, lane, look);
+  while (look.count > 0) {
+#define FFD_SEG_CASE(IDX, WW, RR)                                                   \
+  case IDX: {                                                                       \
+    SegRunner<KIND, D, INT_IN, FIN, WW, RR, ROWS, LO, NSH> run(sm, pb, lane);       \
+    run.stream(look);                                                               \
+    break;                                                                          \
   }
-    switch (it.shape) {
-      FFD_SEG_CASE(0, 16, 2)
-      FFD_SEG_CASE(1, 16, 4)
-      FFD_SEG_CASE(2, 16, 6)
-      FFD_SEG_CASE(3, 16, 8)
-      FFD_SEG_CASE(4, 16, 10)
-      FFD_SEG_CASE(5, 16, 12)
-      FFD_SEG_CASE(6, 16, 14)
-      FFD_SEG_CASE(7, 16, 16)
-      FFD_SEG_CASE(8, 32, 9)
-      FFD_SEG_CASE(9, 32, 10)
-      FFD_SEG_CASE(10, 32, 11)
-      FFD_SEG_CASE(11, 32, 12)
-      FFD_SEG_CASE(12, 32, 13)
-      FFD_SEG_CASE(13, 32, 14)
-      FFD_SEG_CASE(14, 32, 15)
-      FFD_SEG_CASE(15, 32, 16)
-      default:
-        break;
+    if constexpr (BIG) {
+      switch (look.shape) {
+        FFD_SEG_CASE(16, 16, 18)
+        FFD_SEG_CASE(17, 16, 20)
+        FFD_SEG_CASE(18, 16, 22)
+        FFD_SEG_CASE(19, 16, 24)
+        FFD_SEG_CASE(20, 16, 26)
+        FFD_SEG_CASE(21, 16, 28)
+        FFD_SEG_CASE(22, 16, 30)
+        FFD_SEG_CASE(23, 16, 32)
+        default:
+          look.count = 0;
+          break;
+      }
+    } else {
+      switch (look.shape) {
+        FFD_SEG_CASE(0, 16, 2)
+        FFD_SEG_CASE(1, 16, 4)
+        FFD_SEG_CASE(2, 16, 6)
+        FFD_SEG_CASE(3, 16, 8)
+        FFD_SEG_CASE(4, 16, 10)
+        FFD_SEG_CASE(5, 16, 12)
+        FFD_SEG_CASE(6, 16, 14)
+        FFD_SEG_CASE(7, 16, 16)
+        FFD_SEG_CASE(8, 32, 9)
+        FFD_SEG_CASE(9, 32, 10)
+        FFD_SEG_CASE(10, 32, 11)
+        FFD_SEG_CASE(11, 32, 12)
+        FFD_SEG_CASE(12, 32, 13)
+        FFD_SEG_CASE(13, 32, 14)
+        FFD_SEG_CASE(14, 32, 15)
+        FFD_SEG_CASE(15, 32, 16)
+        default:
+          look.count = 0;
+          break;
+      }
     }
 #undef FFD_SEG_CASE
     __syncwarp();
   }
 }
 
-// ---- host side (seg.cu) ------------------------------------------------------
-struct SegWs {
-  PairDesc* sorted;  // [B]
-  SegItem* items;    // [seg_max_items(B)]
-  int* item_off;     // [kSegBins] first item of each bin (descending bin order)
-};
-__host__ __device__ inline int64_t seg_max_items(int64_t B) { return B / 2 + kSegBins + 1; }  // L ≥ 2
-int seg_items_per_segment();  // L: FFD_SEG_L (2 … 8), default kSegL
+// ---- host side (seg.cu, seg_*.cu) -----------------------------------------------
+// launch one instantiation: a persistent grid of SMs × occupancy CTAs (cached per device)
+template <int KIND, int D, bool INT_IN, int FIN, bool BIG>
+cudaError_t seg_launch_one(const SegProblem& pb, int sms, cudaStream_t st) {
+  auto k = seg_kernel<KIND, D, INT_IN, FIN, BIG>;
+  const size_t smem = sizeof(SegSmem<KIND, D, INT_IN, BIG ? kSegRowsBig : kSegRows>) * kWarpsPerCta;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static int occ_cache[64] = {0};
+  int occ = dev < 64 ? occ_cache[dev] : 0;
+  if (occ == 0) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kWarp * kWarpsPerCta, smem);
+    if (occ < 1) occ = 1;
+    if (dev < 64) occ_cache[dev] = occ;
+  }
+  k<<<sms * occ, kWarp * kWarpsPerCta, smem, st>>>(pb);
+  return cudaGetLastError();
+}
+// big: the big kernel (shapes 16–23) first, then the small one
+template <int KIND, int D, bool INT_IN, int FIN>
+cudaError_t seg_launch_k(const SegProblem& pb, int sms, cudaStream_t st, bool big) {
+  if (big) {
+    const cudaError_t e = seg_launch_one<KIND, D, INT_IN, FIN, true>(pb, sms, st);
+    if (e != cudaSuccess) return e;
+  }
+  return seg_launch_one<KIND, D, INT_IN, FIN, false>(pb, sms, st);
+}
+__host__ __device__ inline int64_t seg_max_groups(int64_t B) { return B + kSegBins + 1; }
 // the seg kernel is built for this (kind, dim, int input, finalisation)
 bool seg_supported(int kind, int dim, int int_in, int fin);
-cudaError_t launch_seg(const SegProblem& pb, int kind, int dim, int int_in, int fin, int sms, cudaStream_t st);
+bool seg_big();       // rows above 256 on the big kernel (FFD_SEG_BIG=1)
+cudaError_t launch_seg(const SegProblem& pb, int kind, int dim, int int_in, int fin, int sms, cudaStream_t st,
+                       int64_t* launches);
 
 }  // namespace ffd

@@ -395,7 +395,9 @@ struct SegRunner {
     // one step on positions 2g, 2g+1 of this segment; top0: what the segment's
     // first lane sees above its first row in the first column (the corner 0 on
     // a sentinel, +∞ otherwise; the second column is never a sentinel)
-    auto step = [&](int t, float top0) {
+    const float pass_a = s == 0 ? 0.f : 1.f, pass_b = s == 0 ? finf() : 0.f;
+    auto step = [&](int t, float top0, auto sent_tag) {
+      constexpr bool SENT = decltype(sent_tag)::value;
       const int g = t - s;
       alignas(16) float e0[C::EBYTES / 4], e1[C::EBYTES / 4];
       {
@@ -409,8 +411,18 @@ struct SegRunner {
       }
       const float upv0 = __shfl_up_sync(0xffffffffu, b0v, 1, W);
       const float upv1 = __shfl_up_sync(0xffffffffu, c[R - 1], 1, W);
-      const float up0 = (s == 0) ? top0 : upv0;
-      const float up1 = (s == 0) ? finf() : upv1;
+      float up0, up1;
+      if constexpr (SENT) {
+        up0 = (s == 0) ? top0 : upv0;
+        up1 = (s == 0) ? finf() : upv1;
+      } else {
+        // the segment's first lane sees +∞ above its first row: fma(v, 0, +∞) is
+        // +∞, or NaN when v = +∞, and min3 ignores a NaN operand exactly as it
+        // ignores +∞; every other lane gets fma(v, 1, 0) = v exactly.  (FMA pipe:
+        // a select would take the ALU pipe, the min/max recurrence's bottleneck)
+        up0 = __fmaf_rn(upv0, pass_a, pass_b);
+        up1 = __fmaf_rn(upv1, pass_a, pass_b);
+      }
       float d0[R], d1[R];
       cell_dists<float, KIND, D, R, INT_IN>(x, e0, d0);
       cell_dists<float, KIND, D, R, INT_IN>(x, e1, d1);
@@ -478,7 +490,7 @@ struct SegRunner {
       // step Tk: the sentinel of group k reaches lane 0 (corner value 0 above its first row)
       if (t == next_refill) refill(t);
       if (k > 0) take_rows(x, stage_sa, s == 0);
-      step(t, 0.f);
+      step(t, 0.f, std::true_type{});
       ++t;
       if (k > 0) {
         // the rest of the window: lane s takes group k's rows at step Tk + s; the
@@ -490,7 +502,7 @@ struct SegRunner {
             const int p = s == t - t0;
             res = p ? c[R - 1] : res;
             take_rows(x, stage_sa, p);
-            step(t, finf());
+            step(t, finf(), std::false_type{});
           }
           if (t == next_refill && t < tw) refill(t);
         }
@@ -499,7 +511,7 @@ struct SegRunner {
       while (t < t1) {
         const int stop = min(next_refill, t1);
 #pragma unroll 2
-        for (; t < stop; ++t) step(t, finf());
+        for (; t < stop; ++t) step(t, finf(), std::false_type{});
         if (t == next_refill && t < t1) refill(t);
       }
       if (last) break;
@@ -513,7 +525,7 @@ struct SegRunner {
     // drain: positions past the stream's end reach the last lanes
     for (const int total = t + W - 1; t < total; t++) {
       if (t == next_refill) refill(t);
-      step(t, finf());
+      step(t, finf(), std::false_type{});
     }
     emit(k & SM, c[R - 1]);
     __syncwarp();

@@ -61,7 +61,7 @@ CELL_OF_NORM = {"l1": "f32_d2_l1", "l2": "f32_d2_sq", "linf": "f32_d2_linf"}
 # roofline.traffic (dram bytes per launch of the dominant kernel) is not measurable inside a plain
 # run; it is null here, and the ncu --set full captures of the same kernels, with their dram
 # bytes against the algorithmic bytes, are committed under profiles/ (named per round).
-TRAFFIC_PROFILES = {2: "profiles/r2_c2_batch_ncu_full.txt", 4: "profiles/r2_c4_cdist_ncu_full.txt",
+TRAFFIC_PROFILES = {2: "profiles/r2_c2_seg_ncu_full.txt", 4: "profiles/r2_c4_cdist_ncu_full.txt",
                     5: "profiles/r2_c5_long_ncu_full.txt", 3: "profiles/r1_traffic_c3.csv"}
 
 
@@ -416,8 +416,12 @@ def measure_batch(args, cx, cfg):
     f_meas = (clocks["sm_mhz"] or SM_MAX_MHZ_NOMINAL) * 1e6
     f_max = (clocks["sm_max_mhz"] or SM_MAX_MHZ_NOMINAL) * 1e6
     cell = CELL_OF_CONFIG[cfg.cid]
-    roofline = alu_roofline(cells, kern_max, cell, cx.sms, f_max, f_meas,
-                            f"batch_kernel ({cell} cell)", None)
+    # 2-D batches above 4096 pairs: their single-band pairs (≤ 512 points) run on the
+    # segmented two-column kernel (csrc/seg.cuh), the rest on the batch kernel; the
+    # timed span covers both launches
+    seg = cfg.dim == 2 and B > 4096 and cfg.norm in ("sql2", "l2")
+    kname = (f"seg_kernel + batch_kernel ({cell} cell)" if seg else f"batch_kernel ({cell} cell)")
+    roofline = alu_roofline(cells, kern_max, cell, cx.sms, f_max, f_meas, kname, None)
     roofline["algorithmic_bytes"] = h2d + out.numel() * out.element_size()
     roofline["traffic_ncu"] = TRAFFIC_PROFILES.get(cfg.cid)
     line = {

@@ -419,7 +419,7 @@ def measure_batch(args, cx, cfg):
     # 2-D batches above 4096 pairs: their single-band pairs (≤ 512 points) run on the
     # segmented two-column kernel (csrc/seg.cuh), the rest on the batch kernel; the
     # timed span covers both launches
-    seg = cfg.dim == 2 and B > 4096 and cfg.norm in ("sql2", "l2")
+    seg = B > 4096 and (cfg.dim == 2 or (cfg.dim == 3 and cfg.dtype == "f32" and cfg.norm in ("sql2", "l2")))
     kname = (f"seg_kernel + batch_kernel ({cell} cell)" if seg else f"batch_kernel ({cell} cell)")
     roofline = alu_roofline(cells, kern_max, cell, cx.sms, f_max, f_meas, kname, None)
     roofline["algorithmic_bytes"] = h2d + out.numel() * out.element_size()

@@ -62,7 +62,10 @@
 
 namespace ffd {
 
-constexpr int kLWarps = 8;          // warps (band slots) per CTA
+#ifndef FFD_LWARPS
+#define FFD_LWARPS 8
+#endif
+constexpr int kLWarps = FFD_LWARPS;  // warps (band slots) per CTA
 constexpr int kLSmemRing = 1024;    // slots per intra-CTA link (8 KB; the producer may run
                                     // ~500 steps ahead, far beyond the ~47 the consumer needs)
 constexpr int kLGlobRing = 2048;    // slots per inter-CTA link

@@ -1,8 +1,8 @@
 """Parity of the segmented two-column batch kernel (csrc/seg.cuh) against the CPU oracle.
 
 The segmented kernel takes the single-band Fréchet pairs (longer curve ≤ 512 points,
-period H ≥ W + 32) of batches above 4096 pairs for the 2-D exact-integer squared-L2
-cell and the 2-D fp32 L2 / squared-L2 cells.  Integer results must be bit-exact
+period H ≥ W + 32) of batches above 4096 pairs for every 2-D cell (exact-integer
+sq-L2 / L1 / L∞, fp32 L2 / sq-L2 / L1 / L∞) and the 3-D fp32 L2 / sq-L2 cells.  Integer results must be bit-exact
 against the exact int64 oracle; fp32 results bit-exact against the oracle's fp32
 mirror and within 1e-5 relative of the fp64 oracle.  Shapes cover every (W, R)
 shape, the period limit, items with missing pairs (counts not a multiple of G·L),
@@ -134,3 +134,26 @@ def test_identity_and_translation(ffd):
     shifted = workload.Batch(b.p, b.p + t, np.concatenate([b.offsets[:B_]] * 2),
                              np.concatenate([b.lengths[:B_]] * 2), 2, "sql2")
     assert (ffd.batch(*to_dev(shifted), norm="sql2").cpu().numpy() == 25).all()
+
+
+@pytest.mark.parametrize("norm", ["l1", "linf"])
+def test_l1_linf_f32_and_int(ffd, norm):
+    """the 2-D L1 / L∞ cells (fp32: bit-exact vs the mirror; int32: exact, also outside the window)."""
+    rng = np.random.default_rng(71 + len(norm))
+    lens = rng.integers(1, 601, size=2 * 4500)
+    b = batch_from_lens(rng, lens)
+    check_float(ffd.batch(*to_dev(b), norm=norm).cpu().numpy(), b, norm)
+    bi = batch_from_lens(rng, lens, kind="i")
+    check_int(ffd.batch(*to_dev(bi), norm=norm).cpu().numpy(), bi, norm)
+    bw = batch_from_lens(rng, lens, kind="i", scale=20000.0)
+    bw.p[: bw.p.shape[0] // 2] //= 20000
+    check_int(ffd.batch(*to_dev(bw), norm=norm).cpu().numpy(), bw, norm)
+
+
+@pytest.mark.parametrize("norm", ["l2", "sql2"])
+def test_3d_f32(ffd, norm):
+    """the 3-D fp32 L2 / sq-L2 cell (config 3's dimension), lengths 1..700."""
+    rng = np.random.default_rng(81 + len(norm))
+    lens = rng.integers(1, 701, size=2 * 4300)
+    b = batch_from_lens(rng, lens, dim=3)
+    check_float(ffd.batch(*to_dev(b), norm=norm).cpu().numpy(), b, norm)

@@ -76,6 +76,10 @@ constexpr int kMaxLongCtas = 1024;
 // columns per warp step of the fp32 tier (2 or 4).  Four halve the steps per column but measured
 // slower on config 5 (39.5 against 33 ms per norm: the step time doubled), so two stay the default.
 constexpr int kLCols = FFD_LONG_COLS;
+#ifndef FFD_LONG_UNROLL
+#define FFD_LONG_UNROLL 8  // steps per iteration of the steady loop (8, 4 or 2): config 5 takes
+                           // 93.0 / 94.5 / 98.2 ms per three norms (fewer branch stalls)
+#endif
 #ifndef FFD_LONG_R16
 #define FFD_LONG_R16 1
 #endif
@@ -583,6 +587,22 @@ struct LongRunner {
         for (int k = 0; k < K; k += 2)
           SL::put2(out.ring, out.mask, tbo + (unsigned)(K * gg + k), b[k], b[k + 1], pr, SYS);
       };
+#if FFD_LONG_UNROLL == 8
+#pragma unroll 1
+      for (; t + 8 <= stop; t += 8, g += 8) {
+#pragma unroll
+        for (int u = 0; u < 8; u++) one(g + u);
+      }
+#endif
+#if FFD_LONG_UNROLL >= 4
+#pragma unroll 1
+      for (; t + 4 <= stop; t += 4, g += 4) {
+        one(g);
+        one(g + 1);
+        one(g + 2);
+        one(g + 3);
+      }
+#endif
 #pragma unroll 1
       for (; t + 2 <= stop; t += 2, g += 2) {
         one(g);

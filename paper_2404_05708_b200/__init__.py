@@ -6,7 +6,7 @@ computation runs in the library's CUDA kernels; PyTorch only provides device
 memory and streams.  There is no CPU fallback: if the library or a GPU is
 missing, calls raise.
 
-    batch(p, q, offsets, lengths, norm)        -> Tensor[B]   (ffd_batch)
+    batch(p, q, offsets, lengths, norm)        -> Tensor[B]   (ffd_batch_sized)
     dtw_batch(p, q, offsets, lengths, norm)    -> Tensor[B]   (ffd_batch_dtw)
     dist_sum(p, q, offsets, lengths, norm)     -> Tensor[B] f64 (ffd_dist_sum)
     batch_host(p, q, offsets, lengths, norm)   -> ndarray[B]  (ffd_batch_host)
@@ -54,6 +54,8 @@ def lib():
         P, I64, I32_, SZ = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_size_t
         L.ffd_batch.argtypes = [P, P, P, P, I64, I32_, I32_, I32_, P, P, SZ, P]
         L.ffd_batch.restype = ctypes.c_int
+        L.ffd_batch_sized.argtypes = [P, I64, P, I64, P, P, I64, I32_, I32_, I32_, P, P, SZ, P]
+        L.ffd_batch_sized.restype = ctypes.c_int
         L.ffd_batch_dtw.argtypes = [P, P, P, P, I64, I32_, I32_, I32_, P, P, SZ, P]
         L.ffd_batch_dtw.restype = ctypes.c_int
         L.ffd_batch_dtw_f64.argtypes = [P, P, P, P, I64, I32_, I32_, I32_, P, P, SZ, P]
@@ -95,7 +97,7 @@ def lib():
     return _lib
 
 
-EXPORTED = ["ffd_batch", "ffd_batch_dtw", "ffd_batch_dtw_f64", "ffd_dist_sum", "ffd_batch_workspace_bytes", "ffd_batch_host", "ffd_cdist",
+EXPORTED = ["ffd_batch", "ffd_batch_sized", "ffd_batch_dtw", "ffd_batch_dtw_f64", "ffd_dist_sum", "ffd_batch_workspace_bytes", "ffd_batch_host", "ffd_cdist",
             "ffd_cdist_workspace_bytes", "ffd_cdist_self", "ffd_cdist_to", "ffd_long_pair_ring_bytes",
             "ffd_long_pair_row_align", "ffd_long_pair_shard", "ffd_validate_batch", "ffd_status_string",
             "ffd_take_launch_count", "ffd_version", "ffd_profile_enable", "ffd_profile_take"]
@@ -208,6 +210,11 @@ def batch(p, q, offsets, lengths, norm="l2", out=None, stream=None, measure="fre
         out = torch.empty(B, dtype=odt, device=p.device)
     ws_bytes = lib().ffd_batch_workspace_bytes(B)
     ws = workspace(ws_bytes, p.device, stream)
+    if measure == "frechet":  # the point counts let the library skip the long-pair launch of small batches
+        _check(lib().ffd_batch_sized(p.data_ptr(), p.shape[0], q.data_ptr(), q.shape[0], offsets.data_ptr(),
+                                     lengths.data_ptr(), B, dim, _norm(norm), dt, out.data_ptr(), ws.data_ptr(),
+                                     ws.numel(), _stream_ptr(stream)), "ffd_batch_sized")
+        return out
     fn = getattr(lib(), fns[measure])
     _check(fn(p.data_ptr(), q.data_ptr(), offsets.data_ptr(), lengths.data_ptr(), B, dim,
               _norm(norm), dt, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)), fns[measure])

@@ -371,3 +371,48 @@ def test_l2_tiny_distances_exact(ffd):
     normal = ref >= 2.0 ** -63
     assert np.all(np.abs(got - ref)[normal] <= 1e-5 * np.abs(ref[normal])), (got, ref)
     assert got[vals.index(0.0)] == 0.0
+
+
+def _raw_batch(ffd, p, q, off, lens, norm):
+    """ffd_batch itself (no point counts): the launch chain always ends with the long-pair kernel."""
+    B = off.numel() // 2
+    dt = 1 if p.dtype == torch.int32 else 0
+    out = torch.empty(B, dtype=torch.int64 if dt else torch.float32, device=p.device)
+    ws = torch.empty(int(ffd.lib().ffd_batch_workspace_bytes(B)), dtype=torch.uint8, device=p.device)
+    norms = {"l1": 1, "l2": 2, "linf": 3, "sql2": 4}
+    rc = ffd.lib().ffd_batch(p.data_ptr(), q.data_ptr(), off.data_ptr(), lens.data_ptr(), B, p.shape[1],
+                             norms[norm], dt, out.data_ptr(), ws.data_ptr(), ws.numel(),
+                             torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    return out
+
+
+@pytest.mark.parametrize("long_pair", [False, True])
+def test_batch_sized_skips_long_launch(ffd, long_pair):
+    """ffd_batch_sized (what batch() calls) equals ffd_batch bit for bit; with no
+    pair possibly long (config 1 sizes) it launches one kernel fewer, and with a
+    long pair inside p/q it still runs the long-pair kernel (exact vs the oracle)."""
+    rng = np.random.default_rng(29)
+    if long_pair:
+        lens = rng.integers(1, 200, size=2 * 8).astype(np.int32)
+        lens[3], lens[8 + 3] = 700, 9000
+        b = make_batch(rng, 8, 1, 200, kind="i", lens=lens)
+        norm = "l1"
+    else:
+        b = workload.gen_batch(workload.CONFIGS[1])
+        norm = "l2"
+    p, q, off, lens = to_dev(b)
+    torch.cuda.synchronize()
+    ffd.launches_taken()
+    raw = _raw_batch(ffd, p, q, off, lens, norm)
+    n_raw = ffd.launches_taken()
+    got = ffd.batch(p, q, off, lens, norm=norm, validate=False)
+    n_sized = ffd.launches_taken()
+    torch.cuda.synchronize()
+    assert torch.equal(raw, got)
+    if long_pair:
+        assert n_sized == n_raw
+        assert np.array_equal(got.cpu().numpy(), oracle.batch(b.p, b.q, b.offsets, b.lengths, b.dim, norm))
+    else:
+        assert n_sized == n_raw - 1, (n_raw, n_sized)
+        check_float(got.cpu().numpy(), b, norm)

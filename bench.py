@@ -320,10 +320,12 @@ def measure_batch(args, cx, cfg):
     out = torch.empty(B, dtype=torch.int64 if cfg.dtype == "i32" else torch.float32, device=dev)
     # the inputs are generated by workload/ and checked once by the library's own validator
     assert ffd.validate(p, q, off, lens) == 0
+    # the caller knows its length bounds (ffd_batch_maxlen: no long-pair launch when none can be long)
+    mlen = (int(b.lengths[:B].max()), int(b.lengths[B:].max()))
 
     # ---- device-resident timing ------------------------------------------------
     for _ in range(args.warmup):
-        ffd.batch(p, q, off, lens, norm=cfg.norm, out=out, validate=False)
+        ffd.batch(p, q, off, lens, norm=cfg.norm, out=out, validate=False, max_len=mlen)
     torch.cuda.synchronize()
     ffd.launches_taken()
     ffd.profile_take()
@@ -338,13 +340,13 @@ def measure_batch(args, cx, cfg):
     with sampler:
         if flush:
             ms = timed_steps_flushed(torch, stream, dev,
-                                     lambda: ffd.batch(p, q, off, lens, norm=cfg.norm, out=out, validate=False),
+                                     lambda: ffd.batch(p, q, off, lens, norm=cfg.norm, out=out, validate=False, max_len=mlen),
                                      args.steps)
         else:
             e0.record(stream)
             h0 = time.perf_counter()
             for _ in range(args.steps):
-                ffd.batch(p, q, off, lens, norm=cfg.norm, out=out, validate=False)
+                ffd.batch(p, q, off, lens, norm=cfg.norm, out=out, validate=False, max_len=mlen)
             host_ms = (time.perf_counter() - h0) * 1e3 / args.steps
             e1.record(stream)
             torch.cuda.synchronize()
@@ -368,11 +370,11 @@ def measure_batch(args, cx, cfg):
             side = torch.cuda.Stream(dev)
             side.wait_stream(stream)
             with torch.cuda.stream(side):
-                ffd.batch(p, q, off, lens, norm=cfg.norm, out=out, validate=False)
+                ffd.batch(p, q, off, lens, norm=cfg.norm, out=out, validate=False, max_len=mlen)
             stream.wait_stream(side)
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                ffd.batch(p, q, off, lens, norm=cfg.norm, out=out, validate=False)
+                ffd.batch(p, q, off, lens, norm=cfg.norm, out=out, validate=False, max_len=mlen)
             for _ in range(args.warmup):
                 g.replay()
             torch.cuda.synchronize()
@@ -388,7 +390,7 @@ def measure_batch(args, cx, cfg):
                 g_ms = g0.elapsed_time(g1) / args.steps
             g_ms = cx.reduce([g_ms])[0]
             graph = {"ms_per_step": g_ms, "value": total_cells / (g_ms * 1e-3) / 1e9,
-                     "unit": "Gcells/s", "api": "ffd_batch captured once into a CUDA graph, replayed per step"}
+                     "unit": "Gcells/s", "api": "ffd_batch_maxlen captured once into a CUDA graph, replayed per step"}
         except Exception as e:  # reported, never silently replaced
             graph = {"error": f"{type(e).__name__}: {e}"[:200]}
 
@@ -437,7 +439,8 @@ def measure_batch(args, cx, cfg):
                    "l2": ("L2 flushed (256 MB write) before every timed step; steps timed one by one"
                           if flush else
                           "inputs larger than L2 (%.0f MB per GPU)" % ((b.p.nbytes + b.q.nbytes) / 1e6)),
-                   "parallelism": f"pairs sharded over {cx.ws} GPU(s), no collective on the data path"},
+                   "parallelism": f"pairs sharded over {cx.ws} GPU(s), no collective on the data path",
+                   "api": f"batch() -> ffd_batch_maxlen with the batch's length bounds {list(mlen)}"},
         "clocks": clocks,
         "roofline": roofline,
         "cpu_baseline": cpu_baseline_line(args, cfg, cx.ws),

@@ -84,18 +84,20 @@ int ffd_batch(const void* p, const void* q, const int64_t* offsets, const int32_
               void* workspace, size_t workspace_bytes, ffd_stream_t stream);
 size_t ffd_batch_workspace_bytes(int64_t num_pairs);
 
-/* ffd_batch_sized — ffd_batch with the point counts of p and q (n_p, n_q ≥ 0):
- *   the same operation, arguments, layout, workspace and stream semantics.
- *   Every pair lies inside p and q (ffd_validate_batch checks it), so no pair
- *   is longer than (n_p, n_q); when a pair of that size would not need the
- *   long-pair kernel, its (cooperative, clustered) launch is skipped.  Only a
- *   latency saving for small batches (config 1: 3 → 2 launches); the result is
- *   identical to ffd_batch's.  Offsets out of range are undefined behaviour, as
- *   for ffd_batch; n_p or n_q < 0 → FFD_ERR_ARG.                               */
-int ffd_batch_sized(const void* p, int64_t n_p, const void* q, int64_t n_q, const int64_t* offsets,
-                    const int32_t* lengths, int64_t num_pairs, int32_t dim, int32_t norm,
-                    int32_t dtype, void* out, void* workspace, size_t workspace_bytes,
-                    ffd_stream_t stream);
+/* ffd_batch_maxlen — ffd_batch with caller-known length bounds: every
+ *   lengths[k] ≤ max_n and lengths[B+k] ≤ max_m (k < B; the max_seqlen idea of
+ *   variable-length attention kernels).  Same operation, arguments, layout,
+ *   workspace and stream semantics as ffd_batch.  When no pair within the bounds
+ *   needs the long-pair kernel (pair_goes_long is monotone in the lengths), its
+ *   cooperative clustered launch is skipped: config 1 runs 2 launches instead
+ *   of 3, with results identical to ffd_batch's.  A pair that breaks its bound
+ *   and would need the long-pair kernel gets NaN / INT64_MIN (never a silent
+ *   wrong value); with the point counts of p and q as bounds nothing is ever
+ *   excluded.  max_n or max_m < 0 → FFD_ERR_ARG.                                */
+int ffd_batch_maxlen(const void* p, const void* q, const int64_t* offsets, const int32_t* lengths,
+                     int64_t num_pairs, int64_t max_n, int64_t max_m, int32_t dim, int32_t norm,
+                     int32_t dtype, void* out, void* workspace, size_t workspace_bytes,
+                     ffd_stream_t stream);
 
 /* ffd_batch_dtw — dynamic time warping of B pairs (PAPER Appendix B:
  *   Alg. 2 with max replaced by +, i.e. C[i][j] = min{C[i−1][j], C[i−1][j−1],

@@ -6,7 +6,7 @@ computation runs in the library's CUDA kernels; PyTorch only provides device
 memory and streams.  There is no CPU fallback: if the library or a GPU is
 missing, calls raise.
 
-    batch(p, q, offsets, lengths, norm)        -> Tensor[B]   (ffd_batch_sized)
+    batch(p, q, offsets, lengths, norm)        -> Tensor[B]   (ffd_batch_maxlen)
     dtw_batch(p, q, offsets, lengths, norm)    -> Tensor[B]   (ffd_batch_dtw)
     dist_sum(p, q, offsets, lengths, norm)     -> Tensor[B] f64 (ffd_dist_sum)
     batch_host(p, q, offsets, lengths, norm)   -> ndarray[B]  (ffd_batch_host)
@@ -54,8 +54,8 @@ def lib():
         P, I64, I32_, SZ = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_size_t
         L.ffd_batch.argtypes = [P, P, P, P, I64, I32_, I32_, I32_, P, P, SZ, P]
         L.ffd_batch.restype = ctypes.c_int
-        L.ffd_batch_sized.argtypes = [P, I64, P, I64, P, P, I64, I32_, I32_, I32_, P, P, SZ, P]
-        L.ffd_batch_sized.restype = ctypes.c_int
+        L.ffd_batch_maxlen.argtypes = [P, P, P, P, I64, I64, I64, I32_, I32_, I32_, P, P, SZ, P]
+        L.ffd_batch_maxlen.restype = ctypes.c_int
         L.ffd_batch_dtw.argtypes = [P, P, P, P, I64, I32_, I32_, I32_, P, P, SZ, P]
         L.ffd_batch_dtw.restype = ctypes.c_int
         L.ffd_batch_dtw_f64.argtypes = [P, P, P, P, I64, I32_, I32_, I32_, P, P, SZ, P]
@@ -97,7 +97,7 @@ def lib():
     return _lib
 
 
-EXPORTED = ["ffd_batch", "ffd_batch_sized", "ffd_batch_dtw", "ffd_batch_dtw_f64", "ffd_dist_sum", "ffd_batch_workspace_bytes", "ffd_batch_host", "ffd_cdist",
+EXPORTED = ["ffd_batch", "ffd_batch_maxlen", "ffd_batch_dtw", "ffd_batch_dtw_f64", "ffd_dist_sum", "ffd_batch_workspace_bytes", "ffd_batch_host", "ffd_cdist",
             "ffd_cdist_workspace_bytes", "ffd_cdist_self", "ffd_cdist_to", "ffd_long_pair_ring_bytes",
             "ffd_long_pair_row_align", "ffd_long_pair_shard", "ffd_validate_batch", "ffd_status_string",
             "ffd_take_launch_count", "ffd_version", "ffd_profile_enable", "ffd_profile_take"]
@@ -184,7 +184,8 @@ def _batch_args(p, q, offsets, lengths):
     return dt, p.contiguous(), q.contiguous(), offsets.contiguous(), lengths.contiguous()
 
 
-def batch(p, q, offsets, lengths, norm="l2", out=None, stream=None, measure="frechet", validate=True):
+def batch(p, q, offsets, lengths, norm="l2", out=None, stream=None, measure="frechet", validate=True,
+          max_len=None):
     """δ_dF for B pairs (ffd_batch).  p [Σn, dim], q [Σm, dim] float32/int32 CUDA
     tensors; offsets int64[2B]; lengths int32[2B].  Returns float32[B] (fp32
     input) or int64[B] (int32 input).  measure="dtw": dynamic time warping
@@ -193,7 +194,11 @@ def batch(p, q, offsets, lengths, norm="l2", out=None, stream=None, measure="fre
     runs ffd_validate_batch (synchronous) and raises FFDError on empty curves,
     offsets out of range, non-finite coordinates or int64 overflow; with
     validate=False such pairs give NaN / INT64_MIN (or are undefined).  Inside a
-    CUDA-graph capture the (synchronous) validation is skipped."""
+    CUDA-graph capture the (synchronous) validation is skipped.  max_len: a bound
+    on every curve length (int, or (max p-length, max q-length)); Fréchet calls
+    ffd_batch_maxlen with it (default: the point counts of p and q), which skips
+    the long-pair launch when no pair within it can be long — a pair longer
+    than a bound it breaks gets NaN / INT64_MIN."""
     torch = _torch()
     dt, p, q, offsets, lengths = _batch_args(p, q, offsets, lengths)
     B = offsets.numel() // 2
@@ -210,10 +215,12 @@ def batch(p, q, offsets, lengths, norm="l2", out=None, stream=None, measure="fre
         out = torch.empty(B, dtype=odt, device=p.device)
     ws_bytes = lib().ffd_batch_workspace_bytes(B)
     ws = workspace(ws_bytes, p.device, stream)
-    if measure == "frechet":  # the point counts let the library skip the long-pair launch of small batches
-        _check(lib().ffd_batch_sized(p.data_ptr(), p.shape[0], q.data_ptr(), q.shape[0], offsets.data_ptr(),
-                                     lengths.data_ptr(), B, dim, _norm(norm), dt, out.data_ptr(), ws.data_ptr(),
-                                     ws.numel(), _stream_ptr(stream)), "ffd_batch_sized")
+    if measure == "frechet":  # length bounds let the library skip the long-pair launch of small batches
+        mn, mm = (p.shape[0], q.shape[0]) if max_len is None else (max_len if isinstance(max_len, tuple)
+                                                                   else (max_len, max_len))
+        _check(lib().ffd_batch_maxlen(p.data_ptr(), q.data_ptr(), offsets.data_ptr(), lengths.data_ptr(), B,
+                                      int(mn), int(mm), dim, _norm(norm), dt, out.data_ptr(), ws.data_ptr(),
+                                      ws.numel(), _stream_ptr(stream)), "ffd_batch_maxlen")
         return out
     fn = getattr(lib(), fns[measure])
     _check(fn(p.data_ptr(), q.data_ptr(), offsets.data_ptr(), lengths.data_ptr(), B, dim,

@@ -174,7 +174,8 @@ static int batch_impl(const void* p, const void* q, const int64_t* offsets, cons
   const int out_kind = int_in ? 1 : (measure == 2 ? 2 : 0);
   // single-band Fréchet pairs of the built cells go to the segmented kernel (seg.cuh)
   const bool use_seg = measure == 0 && B > kPrepSmallMax && seg_supported(kind, dim, int_in, fin);
-  if (launch_prep(offsets, lengths, B, out_kind, long_ok, out, ws, di.sms, st, &g_launches, use_seg) !=
+  if (launch_prep(offsets, lengths, B, out_kind, long_ok, out, ws, di.sms, st, &g_launches, use_seg,
+                  long_possible && measure != 2) !=
       cudaSuccess)
     return FFD_ERR_CUDA;
 
@@ -417,16 +418,16 @@ int ffd_batch(const void* p, const void* q, const int64_t* offsets, const int32_
                     workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
 }
 
-int ffd_batch_sized(const void* p, int64_t n_p, const void* q, int64_t n_q, const int64_t* offsets,
-                    const int32_t* lengths, int64_t num_pairs, int32_t dim, int32_t norm,
-                    int32_t dtype, void* out, void* workspace, size_t workspace_bytes,
-                    ffd_stream_t stream) {
-  if (n_p < 0 || n_q < 0) return FFD_ERR_ARG;
-  // pair_goes_long is monotone in (n, m): a pair inside (n_p, n_q) goes long
-  // only if a pair of the full sizes would
+int ffd_batch_maxlen(const void* p, const void* q, const int64_t* offsets, const int32_t* lengths,
+                     int64_t num_pairs, int64_t max_n, int64_t max_m, int32_t dim, int32_t norm,
+                     int32_t dtype, void* out, void* workspace, size_t workspace_bytes,
+                     ffd_stream_t stream) {
+  if (max_n < 0 || max_m < 0) return FFD_ERR_ARG;
+  // pair_goes_long is monotone in (n, m): a pair within the bounds goes long
+  // only if a pair of the bounds' sizes would
   const int64_t cap = int64_t(1) << 30;  // above every threshold, no overflow in the band count
   const bool long_possible =
-      pair_goes_long((int)(n_p < cap ? n_p : cap), (int)(n_q < cap ? n_q : cap),
+      pair_goes_long((int)(max_n < cap ? max_n : cap), (int)(max_m < cap ? max_m : cap),
                      medium_rows_for(num_pairs, dev_info().sms));
   return batch_impl(p, q, offsets, lengths, num_pairs, dim, norm, dtype, out, workspace,
                     workspace_bytes, reinterpret_cast<cudaStream_t>(stream), 0, long_possible);

@@ -88,6 +88,7 @@ constexpr bool kLR16 = FFD_LONG_R16 != 0;  // build the R = 16 bands (fp32 tier)
 // reports the link state with printf, sets the abort flag and gives up
 constexpr long long kWatchdogCycles = 5000000000LL;
 constexpr long long kAbortCheckCycles = 1LL << 20;  // spins read the abort flag only after ~0.5 ms
+constexpr long long kAbortRecheckCycles = 1LL << 15;  // ... and then every ~17 µs
 
 struct LongProblem {
   const void* p;
@@ -175,6 +176,19 @@ __device__ __forceinline__ void st_ctr(unsigned* p, unsigned v) {
 __device__ __forceinline__ bool aborted(const int* abort) {
   return *reinterpret_cast<const volatile int*>(abort) != 0;
 }
+// The abort flag is an L2 round trip: a spin reads it after ~0.5 ms of waiting,
+// then every ~17 µs — not on every poll, where a band waiting out the pipeline
+// fill would see its producer's slot up to one round trip late, a delay that
+// adds up along the chain of bands (round 2: every poll after 0.5 ms read it).
+struct AbortPoll {
+  long long due;
+  __device__ __forceinline__ explicit AbortPoll(long long t0) : due(t0 + kAbortCheckCycles) {}
+  __device__ __forceinline__ bool fired(long long now, const int* abort) {
+    if (now < due) return false;
+    due = now + kAbortRecheckCycles;
+    return aborted(abort);
+  }
+};
 
 // How a DP value of type T moves through {payload, tag} slots.  A = absolute
 // stream position (tag base + position), tag = A + 1.
@@ -419,11 +433,12 @@ struct LongRunner {
     const unsigned want = tb + (unsigned)pos + 1u;
     if (!SL::ready(pre, want)) {
       const long long t0 = clock64();
+      AbortPoll ap(t0);
       while (!SL::ready(pre, want)) {
         pre = SL::load(in.ring, in.mask, tb + (unsigned)pos, in.sys);
-        // the abort flag is an L2 round trip: read it only in a long wait
-        if (clock64() - t0 > kAbortCheckCycles && aborted(pb.abort)) break;
-        if (clock64() - t0 > kWatchdogCycles) {  // a link that never delivers: report, abort
+        const long long now = clock64();
+        if (ap.fired(now, pb.abort)) break;
+        if (now - t0 > kWatchdogCycles) {  // a link that never delivers: report, abort
           printf("ffd long_kernel watchdog: consumer cta %d lane %d pos %d want tag %u (tb %u)\n",
                  (int)blockIdx.x, lane, pos, want, tb);
           atomicExch(pb.abort, 1);
@@ -446,10 +461,12 @@ struct LongRunner {
       const unsigned want = tb + (unsigned)pos + 1u;
       if (!SL::ready(SL::load(in.ring, in.mask, tb + (unsigned)pos, in.sys), want)) {
         const long long t0 = clock64();
+        AbortPoll ap(t0);
         while (!SL::ready(SL::load(in.ring, in.mask, tb + (unsigned)pos, in.sys), want)) {
           __nanosleep(64);
-          if (clock64() - t0 > kAbortCheckCycles && aborted(pb.abort)) break;
-          if (clock64() - t0 > kWatchdogCycles) {
+          const long long now = clock64();
+          if (ap.fired(now, pb.abort)) break;
+          if (now - t0 > kWatchdogCycles) {
             printf("ffd long_kernel watchdog: chunk wait cta %d pos %d want tag %u (tb %u)\n",
                    (int)blockIdx.x, pos, want, tb);
             atomicExch(pb.abort, 1);
@@ -557,11 +574,13 @@ struct LongRunner {
           cons_seen = cons_next;
           if ((int)(cons_seen + cap - (tbo + (unsigned)(K * t))) <= 0) {
             const long long t0 = clock64();
+            AbortPoll ap(t0);
             while ((int)(cons_seen + cap - (tbo + (unsigned)(K * t))) <= 0) {
               __nanosleep(64);
               cons_seen = ld_ctr(out.cons);
-              if (clock64() - t0 > kAbortCheckCycles && aborted(pb.abort)) break;
-              if (clock64() - t0 > kWatchdogCycles) {
+              const long long now = clock64();
+              if (ap.fired(now, pb.abort)) break;
+              if (now - t0 > kWatchdogCycles) {
                 printf("ffd long_kernel watchdog: producer cta %d warp %d t %d cons %u tb %u cap %u\n",
                        (int)blockIdx.x, (int)(threadIdx.x >> 5), t, cons_seen, tbo, cap);
                 atomicExch(pb.abort, 1);

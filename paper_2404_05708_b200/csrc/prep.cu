@@ -75,9 +75,9 @@ __device__ __forceinline__ int pair_key(const int64_t* __restrict__ offsets,
   // DTW (long_ok < 0): only the pairs the batch kernel cannot hold go to the
   // long-pair kernel; Fréchet (long_ok > 0) also sends the medium ones
   if (long_ok == -2 || (long_ok > 0 ? pair_goes_long(n, m, long_ok) : pair_too_long(n, m))) {
-    if (long_ok) {
+    if (long_ok && long_list) {
       long_list[atomicAdd(long_count, 1)] = (int)k;
-    } else {  // no long-pair path requested: NaN
+    } else {  // no long-pair path requested (or its launch ruled out by the caller's length bounds): NaN
       write_invalid(out, k, int_out);
     }
     return -1;
@@ -337,11 +337,12 @@ __global__ void prep_seg_groups_kernel(const int* __restrict__ hist, const int* 
 
 cudaError_t launch_prep(const int64_t* offsets, const int32_t* lengths, int64_t B, int int_out,
                         int long_ok, void* out, const BatchWs& ws, int num_sms, cudaStream_t st,
-                        int64_t* launches, bool seg) {
+                        int64_t* launches, bool seg, bool long_run) {
   if (B == 0) return cudaSuccess;
+  int* const long_list = long_run ? ws.long_list : nullptr;
   if (B <= kPrepSmallMax) {
     prep_small_kernel<<<1, kPrepSmallThreads, 0, st>>>(offsets, lengths, B, int_out, long_ok, out,
-                                                       ws.counters, ws.long_list, ws.sorted);
+                                                       ws.counters, long_list, ws.sorted);
     *launches += 1;
     return cudaGetLastError();
   }
@@ -353,7 +354,7 @@ cudaError_t launch_prep(const int64_t* offsets, const int32_t* lengths, int64_t 
   int64_t blocks = (B + threads - 1) / threads;
   if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
   prep_keys_kernel<<<(int)blocks, threads, 0, st>>>(offsets, lengths, B, int_out, long_ok, out, ws.tmp,
-                                                    ws.keys, ws.hist, ws.long_list,
+                                                    ws.keys, ws.hist, long_list,
                                                     ws.counters + kCtrLong, seg ? (seg_big() ? 2 : 1) : 0);
   if (seg) prep_scan_seg_kernel<<<1, 1024, 0, st>>>(ws.hist, ws.cursor, ws.seg_off, ws.counters);
   else prep_scan_kernel<<<1, kNumKeys, 0, st>>>(ws.hist, ws.cursor, ws.counters + kCtrNumSorted);

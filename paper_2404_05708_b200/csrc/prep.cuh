@@ -76,10 +76,12 @@ struct BatchWs {
 // long_ok: < 0 = DTW (only pairs too long for the bands go to the long-pair list),
 // 0 = no long-pair path (such pairs get NaN / INT64_MIN),
 // else the medium-row threshold (medium_rows_for(B, SMs)) of Fréchet
+// long_run = false: the long-pair kernel will not run (the caller's length
+// bounds rule it out), so a pair that would go long gets NaN / INT64_MIN
 // seg: route the Fréchet pairs the segmented kernel takes (seg_bin ≥ 0) to its
 // list and item table (general path only: B > kPrepSmallMax)
 cudaError_t launch_prep(const int64_t* offsets, const int32_t* lengths, int64_t B, int int_out,
                         int long_ok, void* out, const BatchWs& ws, int num_sms, cudaStream_t st,
-                        int64_t* launches, bool seg = false);
+                        int64_t* launches, bool seg = false, bool long_run = true);
 
 }  // namespace ffd

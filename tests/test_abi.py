@@ -58,10 +58,10 @@ def test_argument_errors_are_synchronous(L):
     assert L.ffd_batch(None, None, None, None, 0, 2, 2, 0, None, None, 0, None) == 0
     # workspace too small
     assert L.ffd_batch(P, P, P, P, 4, 2, 2, 0, P, P, 8, None) == -8
-    # ffd_batch_sized: negative point counts, then the same checks as ffd_batch
-    assert L.ffd_batch_sized(P, -1, P, 4, P, P, 4, 2, 2, 0, P, P, 1 << 30, None) == -1
-    assert L.ffd_batch_sized(P, 4, P, 4, P, P, 4, 5, 2, 0, P, P, 1 << 30, None) == -1
-    assert L.ffd_batch_sized(None, 0, None, 0, None, None, 0, 2, 2, 0, None, None, 0, None) == 0
+    # ffd_batch_maxlen: negative bounds, then the same checks as ffd_batch
+    assert L.ffd_batch_maxlen(P, P, P, P, 4, -1, 4, 2, 2, 0, P, P, 1 << 30, None) == -1
+    assert L.ffd_batch_maxlen(P, P, P, P, 4, 4, 4, 5, 2, 0, P, P, 1 << 30, None) == -1
+    assert L.ffd_batch_maxlen(None, None, None, None, 0, 0, 0, 2, 2, 0, None, None, 0, None) == 0
     # cdist: bad shard / ld_out
     assert L.ffd_cdist(P, 10, 4, P, 10, 4, 2, 2, 0, 5, 3, P, 10, None, 0, None) == -1
     assert L.ffd_cdist(P, 10, 4, P, 10, 4, 2, 2, 0, 0, 10, P, 9, None, 0, None) == -1

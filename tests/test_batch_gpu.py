@@ -387,32 +387,44 @@ def _raw_batch(ffd, p, q, off, lens, norm):
     return out
 
 
-@pytest.mark.parametrize("long_pair", [False, True])
-def test_batch_sized_skips_long_launch(ffd, long_pair):
-    """ffd_batch_sized (what batch() calls) equals ffd_batch bit for bit; with no
-    pair possibly long (config 1 sizes) it launches one kernel fewer, and with a
-    long pair inside p/q it still runs the long-pair kernel (exact vs the oracle)."""
+@pytest.mark.parametrize("case", ["c1_bounded", "long_default", "long_bound_broken"])
+def test_batch_maxlen_skips_long_launch(ffd, case):
+    """ffd_batch_maxlen (what batch() calls): config 1 with its length bounds runs
+    one kernel fewer than ffd_batch, bit-identical; with the default bounds (the
+    point counts) a long pair still runs the long-pair kernel, exact vs the
+    oracle; a long pair that breaks a bound ruling that kernel out gets
+    INT64_MIN, the other pairs stay exact."""
     rng = np.random.default_rng(29)
-    if long_pair:
+    if case == "c1_bounded":
+        b = workload.gen_batch(workload.CONFIGS[1])
+        norm, max_len = "l2", (64, 80)
+        assert b.lengths[:16].max() <= 64 and b.lengths[16:].max() <= 80
+    else:
         lens = rng.integers(1, 200, size=2 * 8).astype(np.int32)
         lens[3], lens[8 + 3] = 700, 9000
         b = make_batch(rng, 8, 1, 200, kind="i", lens=lens)
-        norm = "l1"
-    else:
-        b = workload.gen_batch(workload.CONFIGS[1])
-        norm = "l2"
+        norm, max_len = "l1", (None if case == "long_default" else (200, 200))
     p, q, off, lens = to_dev(b)
     torch.cuda.synchronize()
     ffd.launches_taken()
     raw = _raw_batch(ffd, p, q, off, lens, norm)
     n_raw = ffd.launches_taken()
-    got = ffd.batch(p, q, off, lens, norm=norm, validate=False)
-    n_sized = ffd.launches_taken()
+    got = ffd.batch(p, q, off, lens, norm=norm, validate=False, max_len=max_len)
+    n_got = ffd.launches_taken()
     torch.cuda.synchronize()
-    assert torch.equal(raw, got)
-    if long_pair:
-        assert n_sized == n_raw
-        assert np.array_equal(got.cpu().numpy(), oracle.batch(b.p, b.q, b.offsets, b.lengths, b.dim, norm))
-    else:
-        assert n_sized == n_raw - 1, (n_raw, n_sized)
+    if case == "c1_bounded":
+        assert n_got == n_raw - 1, (n_raw, n_got)
+        assert torch.equal(raw, got)
         check_float(got.cpu().numpy(), b, norm)
+        return
+    ref = oracle.batch(b.p, b.q, b.offsets, b.lengths, b.dim, norm)
+    assert np.array_equal(raw.cpu().numpy(), ref)
+    g = got.cpu().numpy()
+    if case == "long_default":
+        assert n_got == n_raw
+        assert np.array_equal(g, ref)
+    else:
+        assert n_got < n_raw
+        assert g[3] == np.iinfo(np.int64).min
+        keep = np.arange(8) != 3
+        assert np.array_equal(g[keep], ref[keep])

@@ -61,8 +61,8 @@ CELL_OF_NORM = {"l1": "f32_d2_l1", "l2": "f32_d2_sq", "linf": "f32_d2_linf"}
 # roofline.traffic (dram bytes per launch of the dominant kernel) is not measurable inside a plain
 # run; it is null here, and the ncu --set full captures of the same kernels, with their dram
 # bytes against the algorithmic bytes, are committed under profiles/ (named per round).
-TRAFFIC_PROFILES = {2: "profiles/r2_c2_seg_ncu_full.txt", 4: "profiles/r2_c4_cdist_ncu_full.txt",
-                    5: "profiles/r2_c5_long_ncu_full.txt", 3: "profiles/r1_traffic_c3.csv"}
+TRAFFIC_PROFILES = {2: "profiles/r2_traffic_c2.csv", 4: "profiles/r2_c4_cdist_ncu_full.txt",
+                    5: "profiles/r2_traffic_c5.csv", 3: "profiles/r2_traffic_c3.csv"}
 
 
 L2_FLUSH_BELOW = 256 << 20  # inputs smaller than this could stay in L2 (126 MB) between steps
